@@ -1,0 +1,765 @@
+// abi.cu — the C ABI of libqnn.so (include/qnn.h): argument validation, the
+// host half of the paper's QNN canonicalisation — fixed-point
+// multiplier derivation, border-class tables, compile-time folding plans —
+// TMA descriptor encoding, and kernel launches.  No compute happens on the
+// host: every step of the path runs in the kernels of this library.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "../../include/qnn.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace qnn {
+
+static thread_local uint64_t g_launches = 0;
+void count_launch(int n) { g_launches += (uint64_t)n; }
+
+static int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cached[dev] = sms;
+  return sms;
+}
+
+// ---------------------------------------------------------------------------
+// Driver entry points for TMA descriptor encoding (no link against libcuda)
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 p_encode_tiled = nullptr;
+static PFN_cuTensorMapEncodeIm2col_v12000 p_encode_im2col = nullptr;
+static int g_driver_version = 0;
+
+static bool load_driver_entry_points() {
+  static std::once_flag once;
+  static bool ok = false;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = cudaDriverEntryPointSymbolNotFound;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f1, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f2, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+      p_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f1);
+      p_encode_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(f2);
+      ok = true;
+    }
+    cudaDriverGetVersion(&g_driver_version);
+  });
+  return ok;
+}
+
+static CUtensorMapSwizzle swizzle_for(int row_bytes) {
+  return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// Drivers up to 13.1 mis-handle a descriptor flag for tensors under 128 KiB;
+// clear it as the CUDA tooling does for those drivers.
+static void small_tensor_fixup(CUtensorMap* m, unsigned long long bytes) {
+  if (g_driver_version <= 13010 && bytes < 131072ull) reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+}
+
+static bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                      uint32_t box_cols, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {pitch_bytes};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = p_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for((int)box_cols),
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  small_tensor_fixup(m, pitch_bytes * rows);
+  return r == CUDA_SUCCESS;
+}
+
+static bool encode_im2col(CUtensorMap* m, const void* base, int C, int W, int H, int N, uint64_t pitch_bytes,
+                          int lower_w, int lower_h, int upper_w, int upper_h, int BK, int sw, int sh) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {pitch_bytes, pitch_bytes * W, pitch_bytes * W * H};
+  const int lower[2] = {lower_w, lower_h};
+  const int upper[2] = {upper_w, upper_h};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)sw, (cuuint32_t)sh, 1};
+  CUresult r = p_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, lower,
+                               upper, (cuuint32_t)BK, (cuuint32_t)kGemmBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               swizzle_for(BK), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  small_tensor_fixup(m, pitch_bytes * W * H * N);
+  return r == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-point multiplier (reading R2): from the IEEE-754 fields of m,
+// M = round_half_away(significand * 2^31) with significand in [0.5, 1).
+// ---------------------------------------------------------------------------
+static bool derive_multiplier(double m, int32_t* M, int32_t* shift) {
+  if (!(m > 0.0) || !std::isfinite(m)) return false;
+  uint64_t bits;
+  std::memcpy(&bits, &m, sizeof(bits));
+  const int biased = (int)((bits >> 52) & 0x7FF);
+  if (biased == 0) {  // subnormal: renormalise through frexp
+    int e = 0;
+    const double sig = std::frexp(m, &e);
+    int64_t Mi = (int64_t)std::floor(std::ldexp(sig, 31) + 0.5);
+    if (Mi == (int64_t)1 << 31) {
+      Mi >>= 1;
+      ++e;
+    }
+    *M = (int32_t)Mi;
+    *shift = e;
+    return true;
+  }
+  const uint64_t mant = (bits & ((1ull << 52) - 1)) | (1ull << 52);  // in [2^52, 2^53)
+  int e = biased - 1023 + 1;                                          // m = (mant / 2^53) * 2^e
+  uint64_t Mi = (mant + (1ull << 21)) >> 22;                          // round half up (= away, m > 0)
+  if (Mi == (1ull << 31)) {
+    Mi = 1ull << 30;
+    ++e;
+  }
+  *M = (int32_t)Mi;
+  *shift = e;
+  return true;
+}
+
+// multiplier -> (M, right shift) for the kernels; rsh >= 63 rounds every int32 product to 0
+static bool kernel_multiplier(double m, int32_t* M, int32_t* rsh) {
+  int32_t Mi, sh;
+  if (!derive_multiplier(m, &Mi, &sh)) return false;
+  const int r = 31 - sh;
+  if (r < 1) return false;  // m >= 2^30: unsupported (reading R15)
+  if (r > 62) {
+    *M = 0;
+    *rsh = 1;
+  } else {
+    *M = Mi;
+    *rsh = r;
+  }
+  return true;
+}
+
+static bool dtype_range(qnn_dtype_t dt, int64_t* lo, int64_t* hi) {
+  switch (dt) {
+    case QNN_S8: *lo = -128; *hi = 127; return true;
+    case QNN_U8: *lo = 0; *hi = 255; return true;
+    case QNN_S32: *lo = INT32_MIN; *hi = INT32_MAX; return true;
+    default: return false;
+  }
+}
+static bool is_8bit(qnn_dtype_t dt) { return dt == QNN_S8 || dt == QNN_U8; }
+static bool zp_ok(qnn_dtype_t dt, int32_t zp) {
+  int64_t lo, hi;
+  return dtype_range(dt, &lo, &hi) && zp >= lo && zp <= hi;
+}
+static bool scale_ok(float s) { return std::isfinite(s) && s > 0.0f; }
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// Conv plan: everything the host derives from the descriptor
+// ---------------------------------------------------------------------------
+struct ConvPlan {
+  bool depthwise = false;
+  int P = 0, Q = 0;
+  long long M = 0;
+  int in_cs = 0, out_cs = 0;
+  // tensor-core path
+  bool pad_copy = false;
+  int Ct = 0;            // channel count / pitch seen by TMA
+  int BK = 0, nchunks = 0, Cw = 0, BN = 0, Kpad = 0, num_n = 0, num_m = 0, stages = 0;
+  bool im2col = false;
+  ClassTable ct{};
+  std::vector<uint8_t> rowcls, colcls;
+  // epilogue
+  bool requant = false;
+  int32_t lo = 0, hi = 0, zp_out = 0;
+  int mode = 0;
+  qnn_dtype_t out_dt = QNN_S32;
+  // packed blob layout
+  size_t pk_w = 0, pk_off = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
+  // workspace layout
+  size_t ws_pad = 0, ws_pixsum = 0, ws_rowsum = 0, ws_total = 0;
+};
+
+static qnn_status_t build_classes(int out, int in, int ksz, int stride, int pad, int dil, int* lo, int* hi, int* ncls,
+                                  std::vector<uint8_t>& cls) {
+  std::map<std::pair<int, int>, int> ids;
+  cls.assign(out, 0);
+  for (int p = 0; p < out; ++p) {
+    int a = ksz, b = -1;
+    for (int r = 0; r < ksz; ++r) {
+      const long long h = (long long)p * stride + (long long)r * dil - pad;
+      if (h >= 0 && h < in) {
+        a = std::min(a, r);
+        b = std::max(b, r);
+      }
+    }
+    if (b < 0) {
+      a = 0;
+      b = -1;
+    }
+    auto key = std::make_pair(a, b);
+    auto it = ids.find(key);
+    int id;
+    if (it == ids.end()) {
+      id = (int)ids.size();
+      if (id >= 32) return QNN_ERR_UNSUPPORTED;
+      ids[key] = id;
+      lo[id] = a;
+      hi[id] = b;
+    } else {
+      id = it->second;
+    }
+    cls[p] = (uint8_t)id;
+  }
+  *ncls = (int)ids.size();
+  return QNN_OK;
+}
+
+static qnn_status_t validate_output(const qnn_output_params_t* o, ConvPlan& pl) {
+  if (!o) {
+    pl.requant = false;
+    pl.out_dt = QNN_S32;
+    pl.lo = INT32_MIN;
+    pl.hi = INT32_MAX;
+    return QNN_OK;
+  }
+  if (!is_8bit(o->out_dtype)) return QNN_ERR_UNSUPPORTED;
+  if (!scale_ok(o->output_scale) || !zp_ok(o->out_dtype, o->output_zero_point)) return QNN_ERR_INVALID_VALUE;
+  if (o->rounding != QNN_ROUND_UPWARD && o->rounding != QNN_ROUND_TONEAREST) return QNN_ERR_INVALID_VALUE;
+  int64_t qlo, qhi;
+  dtype_range(o->out_dtype, &qlo, &qhi);
+  int64_t lo = std::max<int64_t>(qlo, o->act_min);
+  if (o->relu) lo = std::max<int64_t>(lo, o->output_zero_point);
+  const int64_t hi = std::min<int64_t>(qhi, o->act_max);
+  if (lo > hi) return QNN_ERR_INVALID_VALUE;
+  pl.requant = true;
+  pl.out_dt = o->out_dtype;
+  pl.lo = (int32_t)lo;
+  pl.hi = (int32_t)hi;
+  pl.zp_out = o->output_zero_point;
+  pl.mode = (int)o->rounding;
+  return QNN_OK;
+}
+
+static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, ConvPlan& pl,
+                             bool need_scales = true) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  if (d->N <= 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->K <= 0 || d->R <= 0 || d->S <= 0)
+    return QNN_ERR_INVALID_VALUE;
+  if (d->stride_h <= 0 || d->stride_w <= 0 || d->dil_h <= 0 || d->dil_w <= 0 || d->groups <= 0)
+    return QNN_ERR_INVALID_VALUE;
+  if (d->pad_t < 0 || d->pad_l < 0 || d->pad_b < 0 || d->pad_r < 0) return QNN_ERR_INVALID_VALUE;
+  if (!is_8bit(d->input_dtype) || !is_8bit(d->kernel_dtype)) return QNN_ERR_UNSUPPORTED;
+  if (!zp_ok(d->input_dtype, d->input_zero_point) || !zp_ok(d->kernel_dtype, d->kernel_zero_point))
+    return QNN_ERR_INVALID_VALUE;
+  if (d->C % d->groups != 0 || d->K % d->groups != 0) return QNN_ERR_INVALID_VALUE;
+  pl.depthwise = d->groups > 1;
+  if (pl.depthwise && !(d->groups == d->C && d->K == d->C)) return QNN_ERR_UNSUPPORTED;
+  const long long Pn = ((long long)d->H + d->pad_t + d->pad_b - (long long)d->dil_h * (d->R - 1) - 1) / d->stride_h + 1;
+  const long long Qn = ((long long)d->W + d->pad_l + d->pad_r - (long long)d->dil_w * (d->S - 1) - 1) / d->stride_w + 1;
+  if (d->H + d->pad_t + d->pad_b < (long long)d->dil_h * (d->R - 1) + 1 ||
+      d->W + d->pad_l + d->pad_r < (long long)d->dil_w * (d->S - 1) + 1 || Pn <= 0 || Qn <= 0)
+    return QNN_ERR_INVALID_VALUE;
+  pl.P = (int)Pn;
+  pl.Q = (int)Qn;
+  pl.M = (long long)d->N * Pn * Qn;
+  if (pl.M > INT32_MAX) return QNN_ERR_UNSUPPORTED;
+  pl.in_cs = d->in_cstride ? d->in_cstride : d->C;
+  pl.out_cs = d->out_cstride ? d->out_cstride : d->K;
+  if (pl.in_cs < d->C || pl.out_cs < d->K) return QNN_ERR_INVALID_VALUE;
+  // reading R10: int32 exactness of the accumulator
+  const long long KK = (long long)(d->C / d->groups) * d->R * d->S;
+  if (KK * 255LL * 255LL > (long long)INT32_MAX) return QNN_ERR_UNSUPPORTED;
+  // scales
+  if (!scale_ok(d->input_scale)) return QNN_ERR_INVALID_VALUE;
+  if (o && need_scales) {
+    if (!d->kernel_scales || !(d->num_kernel_scales == 1 || d->num_kernel_scales == d->K)) return QNN_ERR_INVALID_VALUE;
+    for (int i = 0; i < d->num_kernel_scales; ++i)
+      if (!scale_ok(d->kernel_scales[i])) return QNN_ERR_INVALID_VALUE;
+  }
+  qnn_status_t st = validate_output(o, pl);
+  if (st != QNN_OK) return st;
+
+  if (pl.depthwise) {
+    const int C = d->C, RS = d->R * d->S;
+    size_t off = 0;
+    pl.pk_w = off;
+    off = align256(off + (size_t)RS * C * 2);
+    pl.pk_bias = off;
+    off = align256(off + (size_t)C * 4);
+    pl.pk_mult = off;
+    off = align256(off + (size_t)C * 4);
+    pl.pk_rsh = off;
+    off = align256(off + (size_t)C * 4);
+    pl.pk_total = off;
+    pl.ws_total = 0;
+    return QNN_OK;
+  }
+
+  // ------------------------------------------------------------ tensor-core plan
+  const bool tma_pitch_ok = (pl.in_cs % 16) == 0;
+  pl.pad_copy = !tma_pitch_ok;
+  pl.Ct = pl.pad_copy ? round_up(d->C, 16) : d->C;
+  {
+    int best_bk = 128, best = INT32_MAX;
+    for (int bk : {128, 64, 32}) {
+      const int n = (pl.Ct + bk - 1) / bk;
+      if (n * bk < best) {
+        best = n * bk;
+        best_bk = bk;
+      }
+    }
+    pl.BK = best_bk;
+    pl.nchunks = (pl.Ct + best_bk - 1) / best_bk;
+    pl.Cw = pl.nchunks * best_bk;
+  }
+  pl.num_n = (d->K + 255) / 256;
+  pl.BN = round_up((d->K + pl.num_n - 1) / pl.num_n, 32);
+  pl.Kpad = pl.num_n * pl.BN;
+  pl.num_m = (int)((pl.M + kGemmBM - 1) / kGemmBM);
+  pl.stages = gemm_max_stages(pl.BK, pl.BN);
+  pl.im2col = !(d->R == 1 && d->S == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_t == 0 && d->pad_l == 0 &&
+                 d->pad_b == 0 && d->pad_r == 0);
+  if (pl.im2col) {
+    const int lw = -d->pad_l, lh = -d->pad_t;
+    const int uw = d->pad_r - (d->S - 1) * d->dil_w, uh = d->pad_b - (d->R - 1) * d->dil_h;
+    if (lw < -128 || lh < -128 || uw < -128 || uh < -128 || uw > 127 || uh > 127) return QNN_ERR_UNSUPPORTED;
+    if ((d->R - 1) * d->dil_h > 255 || (d->S - 1) * d->dil_w > 255) return QNN_ERR_UNSUPPORTED;
+    if (d->stride_h > 8 || d->stride_w > 8) return QNN_ERR_UNSUPPORTED;
+  }
+  st = build_classes(pl.P, d->H, d->R, d->stride_h, d->pad_t, d->dil_h, pl.ct.r_lo, pl.ct.r_hi, &pl.ct.ncr, pl.rowcls);
+  if (st != QNN_OK) return st;
+  st = build_classes(pl.Q, d->W, d->S, d->stride_w, d->pad_l, d->dil_w, pl.ct.s_lo, pl.ct.s_hi, &pl.ct.ncc, pl.colcls);
+  if (st != QNN_OK) return st;
+  if (pl.ct.ncr * pl.ct.ncc > 255) return QNN_ERR_UNSUPPORTED;
+
+  const int RS = d->R * d->S;
+  size_t off = 0;
+  pl.pk_w = off;
+  off = align256(off + (size_t)pl.Kpad * RS * pl.Cw);
+  pl.pk_off = off;
+  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
+  pl.pk_mult = off;
+  off = align256(off + (size_t)pl.Kpad * 4);
+  pl.pk_rsh = off;
+  off = align256(off + (size_t)pl.Kpad * 4);
+  pl.pk_rowcls = off;
+  off = align256(off + (size_t)pl.P);
+  pl.pk_colcls = off;
+  off = align256(off + (size_t)pl.Q);
+  pl.pk_total = off;
+
+  size_t w = 0;
+  if (pl.pad_copy) {
+    pl.ws_pad = w;
+    w = align256(w + (size_t)d->N * d->H * d->W * pl.Ct);
+  }
+  if (d->kernel_zero_point != 0) {
+    pl.ws_pixsum = w;
+    w = align256(w + (size_t)d->N * d->H * d->W * 4);
+    pl.ws_rowsum = w;
+    w = align256(w + (size_t)pl.M * 4);
+  }
+  pl.ws_total = w;
+  return QNN_OK;
+}
+
+static qnn_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? QNN_OK : QNN_ERR_CUDA; }
+
+static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel, const int32_t* bias,
+                                 const qnn_output_params_t* o, void* packed, size_t packed_bytes, cudaStream_t s) {
+  ConvPlan pl;
+  qnn_status_t st = make_plan(d, o, pl);
+  if (st != QNN_OK) return st;
+  if (!kernel || !packed) return QNN_ERR_INVALID_VALUE;
+  if (packed_bytes < pl.pk_total) return QNN_ERR_WORKSPACE;
+  if (reinterpret_cast<uintptr_t>(packed) & 255) return QNN_ERR_MISALIGNED;
+  uint8_t* pk = reinterpret_cast<uint8_t*>(packed);
+  const int w_signed = d->kernel_dtype == QNN_S8;
+
+  // per-channel multipliers m_k = s_A * s_W[k] / s_out (reading R3)
+  const int nmult = pl.depthwise ? d->C : pl.Kpad;
+  std::vector<int32_t> mult(nmult, 0), rsh(nmult, 1);
+  if (pl.requant) {
+    for (int k = 0; k < d->K; ++k) {
+      const double m = ((double)d->input_scale * (double)d->kernel_scales[d->num_kernel_scales == 1 ? 0 : k]) /
+                       (double)o->output_scale;
+      if (!kernel_multiplier(m, &mult[k], &rsh[k])) return QNN_ERR_UNSUPPORTED;
+    }
+  }
+  cudaError_t e;
+  if (pl.depthwise) {
+    e = launch_pack_dw_weights(kernel, w_signed, d->kernel_zero_point, reinterpret_cast<int16_t*>(pk + pl.pk_w), d->C,
+                               d->R * d->S, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    if (bias)
+      e = cudaMemcpyAsync(pk + pl.pk_bias, bias, (size_t)d->C * 4, cudaMemcpyDeviceToDevice, s);
+    else
+      e = cudaMemsetAsync(pk + pl.pk_bias, 0, (size_t)d->C * 4, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+  } else {
+    e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
+                            pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off), pl.Kpad, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    e = cudaMemcpyAsync(pk + pl.pk_rowcls, pl.rowcls.data(), pl.rowcls.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(pk + pl.pk_colcls, pl.colcls.data(), pl.colcls.size(), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+  }
+  e = cudaMemcpyAsync(pk + pl.pk_mult, mult.data(), mult.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(pk + pl.pk_rsh, rsh.data(), rsh.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die on return
+  return cuda_status(e);
+}
+
+static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, const void* packed,
+                                const void* input, void* output, void* ws, size_t ws_bytes, cudaStream_t s) {
+  ConvPlan pl;
+  qnn_status_t st = make_plan(d, o, pl, /*need_scales=*/false);
+  if (st != QNN_OK) return st;
+  if (!packed || !input || !output) return QNN_ERR_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(packed) & 255) return QNN_ERR_MISALIGNED;
+  if (pl.ws_total && (!ws || ws_bytes < pl.ws_total)) return QNN_ERR_WORKSPACE;
+  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255)) return QNN_ERR_MISALIGNED;
+  const uint8_t* pk = reinterpret_cast<const uint8_t*>(packed);
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  const int a_signed = d->input_dtype == QNN_S8;
+
+  if (pl.depthwise) {
+    DwParams p{};
+    p.in = input;
+    p.w = reinterpret_cast<const int16_t*>(pk + pl.pk_w);
+    p.bias = reinterpret_cast<const int32_t*>(pk + pl.pk_bias);
+    p.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
+    p.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
+    p.out = output;
+    p.in_cstride = pl.in_cs;
+    p.out_cstride = pl.out_cs;
+    p.N = d->N; p.H = d->H; p.W = d->W; p.C = d->C; p.P = pl.P; p.Q = pl.Q; p.R = d->R; p.S = d->S;
+    p.sh = d->stride_h; p.sw = d->stride_w; p.pt = d->pad_t; p.pl = d->pad_l; p.dh = d->dil_h; p.dw = d->dil_w;
+    p.a_signed = a_signed;
+    p.zpA = d->input_zero_point;
+    p.out_dtype = pl.requant ? (int)pl.out_dt : DT_S32;
+    p.requant = pl.requant;
+    p.mode = pl.mode;
+    p.zp_out = pl.zp_out; p.lo = pl.lo; p.hi = pl.hi;
+    return cuda_status(launch_depthwise(p, s));
+  }
+
+  if (reinterpret_cast<uintptr_t>(input) & 15) return QNN_ERR_MISALIGNED;
+  if (!load_driver_entry_points()) return QNN_ERR_CUDA;
+  cudaError_t e;
+  const void* A = input;
+  long long a_pitch = pl.in_cs;
+  if (pl.pad_copy) {
+    e = launch_pad_channels(input, pl.in_cs, wsb + pl.ws_pad, pl.Ct, (long long)d->N * d->H * d->W, d->C, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    A = wsb + pl.ws_pad;
+    a_pitch = pl.Ct;
+  }
+  const int32_t* rowsum = nullptr;
+  if (d->kernel_zero_point != 0) {
+    int32_t* pixsum = reinterpret_cast<int32_t*>(wsb + pl.ws_pixsum);
+    e = launch_pixel_sums(input, a_signed, pl.in_cs, d->C, (long long)d->N * d->H * d->W, pixsum, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    if (!pl.im2col) {
+      rowsum = pixsum;  // 1x1 / stride 1 / no padding: one pixel per row
+    } else {
+      int32_t* rs = reinterpret_cast<int32_t*>(wsb + pl.ws_rowsum);
+      e = launch_window_sums(pixsum, d->N, d->H, d->W, pl.P, pl.Q, d->R, d->S, d->stride_h, d->stride_w, d->pad_t,
+                             d->pad_l, d->dil_h, d->dil_w, rs, s);
+      if (e != cudaSuccess) return QNN_ERR_CUDA;
+      rowsum = rs;
+    }
+  }
+
+  alignas(64) CUtensorMap tmA, tmB;
+  bool ok;
+  if (pl.im2col)
+    ok = encode_im2col(&tmA, A, pl.pad_copy ? pl.Ct : d->C, d->W, d->H, d->N, (uint64_t)a_pitch, -d->pad_l, -d->pad_t,
+                       d->pad_r - (d->S - 1) * d->dil_w, d->pad_b - (d->R - 1) * d->dil_h, pl.BK, d->stride_w,
+                       d->stride_h);
+  else
+    ok = encode_2d(&tmA, A, (uint64_t)(pl.pad_copy ? pl.Ct : d->C), (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmBM);
+  if (!ok) return QNN_ERR_UNSUPPORTED;
+  ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)d->R * d->S * pl.Cw, (uint64_t)pl.Kpad,
+                 (uint64_t)d->R * d->S * pl.Cw, pl.BK, pl.BN);
+  if (!ok) return QNN_ERR_UNSUPPORTED;
+
+  GemmParams p{};
+  p.M = (int)pl.M;
+  p.Nout = d->K;
+  p.nchunks = pl.nchunks;
+  p.num_kb = d->R * d->S * pl.nchunks;
+  p.S = d->S;
+  p.dil_h = d->dil_h;
+  p.dil_w = d->dil_w;
+  p.BK = pl.BK;
+  p.BN = pl.BN;
+  p.stages = pl.stages;
+  p.num_m_tiles = pl.num_m;
+  p.num_n_tiles = pl.num_n;
+  p.im2col = pl.im2col;
+  p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = d->stride_w; p.pt = d->pad_t; p.pl = d->pad_l;
+  p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8, kGemmBM, pl.BN);
+  GemmEpilogue& ep = p.e;
+  ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
+  ep.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
+  ep.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
+  const bool one_class = pl.ct.ncr * pl.ct.ncc == 1;
+  ep.rowcls = one_class ? nullptr : pk + pl.pk_rowcls;
+  ep.colcls = one_class ? nullptr : pk + pl.pk_colcls;
+  ep.ncc = pl.ct.ncc;
+  ep.rowsum = rowsum;
+  ep.zpW = d->kernel_zero_point;
+  ep.out = output;
+  ep.out_pitch = pl.out_cs;
+  ep.Kpad = pl.Kpad;
+  ep.out_dtype = pl.requant ? (int)pl.out_dt : DT_S32;
+  ep.requant = pl.requant;
+  ep.mode = pl.mode;
+  ep.zp_out = pl.zp_out;
+  ep.lo = pl.lo;
+  ep.hi = pl.hi;
+  const int tiles = pl.num_m * pl.num_n;
+  const int grid = std::min(tiles, sm_count());
+  return cuda_status(launch_gemm(tmA, tmB, p, grid, s));
+}
+
+// dense -> 1x1 conv over an M x 1 x 1 "image batch"
+static qnn_conv2d_desc_t dense_as_conv(const qnn_dense_desc_t* d) {
+  qnn_conv2d_desc_t c{};
+  c.N = d->M; c.H = 1; c.W = 1; c.C = d->K; c.K = d->N; c.R = 1; c.S = 1;
+  c.stride_h = c.stride_w = 1; c.dil_h = c.dil_w = 1; c.groups = 1;
+  c.in_cstride = d->lda; c.out_cstride = d->ldc;
+  c.input_dtype = d->a_dtype; c.kernel_dtype = d->w_dtype;
+  c.input_zero_point = d->zp_A; c.kernel_zero_point = d->zp_W;
+  c.input_scale = d->s_A; c.kernel_scales = d->s_W; c.num_kernel_scales = d->n_sW;
+  return c;
+}
+
+static qnn_status_t shape_info(const int64_t* shape, int32_t ndim, int32_t axis, long long* count, long long* inner,
+                               int* cext) {
+  if (!shape || ndim < 1 || ndim > 8) return QNN_ERR_INVALID_VALUE;
+  if (axis < 0) axis += ndim;
+  if (axis < 0 || axis >= ndim) return QNN_ERR_INVALID_VALUE;
+  long long c = 1, in = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (shape[i] < 0) return QNN_ERR_INVALID_VALUE;
+    c *= shape[i];
+    if (i > axis) in *= shape[i];
+  }
+  *count = c;
+  *inner = in > 0 ? in : 1;
+  *cext = (int)shape[axis];
+  return QNN_OK;
+}
+
+}  // namespace qnn
+
+using namespace qnn;
+
+extern "C" {
+
+const char* qnn_status_string(qnn_status_t st) {
+  switch (st) {
+    case QNN_OK: return "QNN_OK";
+    case QNN_ERR_INVALID_VALUE: return "QNN_ERR_INVALID_VALUE";
+    case QNN_ERR_UNSUPPORTED: return "QNN_ERR_UNSUPPORTED";
+    case QNN_ERR_MISALIGNED: return "QNN_ERR_MISALIGNED";
+    case QNN_ERR_WORKSPACE: return "QNN_ERR_WORKSPACE";
+    case QNN_ERR_CUDA: return "QNN_ERR_CUDA";
+  }
+  return "QNN_ERR_UNKNOWN";
+}
+
+uint64_t qnn_launch_counter(void) { return g_launches; }
+void qnn_launch_counter_reset(void) { g_launches = 0; }
+
+qnn_status_t qnn_derive_multiplier(double m, int32_t* M, int32_t* shift) {
+  if (!M || !shift) return QNN_ERR_INVALID_VALUE;
+  return derive_multiplier(m, M, shift) ? QNN_OK : QNN_ERR_INVALID_VALUE;
+}
+
+qnn_status_t qnn_conv2d_prepack_size(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, size_t* bytes) {
+  if (!bytes) return QNN_ERR_INVALID_VALUE;
+  ConvPlan pl;
+  qnn_status_t st = make_plan(d, o, pl, false);
+  if (st == QNN_OK) *bytes = pl.pk_total;
+  return st;
+}
+
+qnn_status_t qnn_conv2d_prepack(const qnn_conv2d_desc_t* d, const void* kernel, const int32_t* bias,
+                                const qnn_output_params_t* o, void* packed, size_t packed_bytes, qnn_stream_t stream) {
+  return conv_prepack(d, kernel, bias, o, packed, packed_bytes, (cudaStream_t)stream);
+}
+
+qnn_status_t qnn_conv2d_workspace_size(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, size_t* bytes) {
+  if (!bytes) return QNN_ERR_INVALID_VALUE;
+  ConvPlan pl;
+  qnn_status_t st = make_plan(d, o, pl, false);
+  if (st == QNN_OK) *bytes = pl.ws_total;
+  return st;
+}
+
+qnn_status_t qnn_conv2d_packed(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, const void* packed,
+                               const void* input, void* output, void* workspace, size_t workspace_bytes,
+                               qnn_stream_t stream) {
+  return conv_packed(d, o, packed, input, output, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+qnn_status_t qnn_conv2d(const qnn_conv2d_desc_t* d, const void* input, const void* kernel, const int32_t* bias,
+                        const qnn_output_params_t* o, void* output, void* workspace, size_t workspace_bytes,
+                        qnn_stream_t stream) {
+  ConvPlan pl;
+  qnn_status_t st = make_plan(d, o, pl, true);
+  if (st != QNN_OK) return st;
+  const size_t pk = align256(pl.pk_total);
+  if (!workspace || workspace_bytes < pk + pl.ws_total) return QNN_ERR_WORKSPACE;
+  st = conv_prepack(d, kernel, bias, o, workspace, pk, (cudaStream_t)stream);
+  if (st != QNN_OK) return st;
+  uint8_t* rest = reinterpret_cast<uint8_t*>(workspace) + pk;
+  return conv_packed(d, o, workspace, input, output, pl.ws_total ? rest : nullptr, workspace_bytes - pk,
+                     (cudaStream_t)stream);
+}
+
+qnn_status_t qnn_depthwise_conv2d(const qnn_conv2d_desc_t* d, const void* input, const void* kernel,
+                                  const int32_t* bias, const qnn_output_params_t* o, void* output, void* workspace,
+                                  size_t workspace_bytes, qnn_stream_t stream) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  if (!(d->groups == d->C && d->K == d->C && d->groups > 1)) return QNN_ERR_INVALID_VALUE;
+  return qnn_conv2d(d, input, kernel, bias, o, output, workspace, workspace_bytes, stream);
+}
+
+qnn_status_t qnn_dense_prepack_size(const qnn_dense_desc_t* d, const qnn_output_params_t* o, size_t* bytes) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  const qnn_conv2d_desc_t c = dense_as_conv(d);
+  return qnn_conv2d_prepack_size(&c, o, bytes);
+}
+qnn_status_t qnn_dense_prepack(const qnn_dense_desc_t* d, const void* W, const int32_t* bias,
+                               const qnn_output_params_t* o, void* packed, size_t packed_bytes, qnn_stream_t stream) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  const qnn_conv2d_desc_t c = dense_as_conv(d);
+  return qnn_conv2d_prepack(&c, W, bias, o, packed, packed_bytes, stream);
+}
+qnn_status_t qnn_dense_workspace_size(const qnn_dense_desc_t* d, const qnn_output_params_t* o, size_t* bytes) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  const qnn_conv2d_desc_t c = dense_as_conv(d);
+  return qnn_conv2d_workspace_size(&c, o, bytes);
+}
+qnn_status_t qnn_dense_packed(const qnn_dense_desc_t* d, const qnn_output_params_t* o, const void* packed,
+                              const void* A, void* out, void* workspace, size_t workspace_bytes, qnn_stream_t stream) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  const qnn_conv2d_desc_t c = dense_as_conv(d);
+  return qnn_conv2d_packed(&c, o, packed, A, out, workspace, workspace_bytes, stream);
+}
+qnn_status_t qnn_dense(const qnn_dense_desc_t* d, const void* A, const void* W, const int32_t* bias,
+                       const qnn_output_params_t* o, void* out, void* workspace, size_t workspace_bytes,
+                       qnn_stream_t stream) {
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  const qnn_conv2d_desc_t c = dense_as_conv(d);
+  return qnn_conv2d(&c, A, W, bias, o, out, workspace, workspace_bytes, stream);
+}
+
+qnn_status_t qnn_requantize(const void* in, qnn_dtype_t in_dtype, void* out, qnn_dtype_t out_dtype,
+                            const int64_t* shape, int32_t ndim, int32_t axis, const float* in_scales,
+                            int32_t n_in_scales, int32_t in_zp, float out_scale, int32_t out_zp,
+                            qnn_rounding_t rounding, qnn_stream_t stream) {
+  static RequantParams p;  // large (20 KB): keep off the stack; guarded below
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  long long count, inner;
+  int cext;
+  qnn_status_t st = shape_info(shape, ndim, axis, &count, &inner, &cext);
+  if (st != QNN_OK) return st;
+  int64_t lo, hi;
+  if (!dtype_range(in_dtype, &lo, &hi) || !dtype_range(out_dtype, &lo, &hi)) return QNN_ERR_UNSUPPORTED;
+  if (!zp_ok(in_dtype, in_zp) || !zp_ok(out_dtype, out_zp)) return QNN_ERR_INVALID_VALUE;
+  if (rounding != QNN_ROUND_UPWARD && rounding != QNN_ROUND_TONEAREST) return QNN_ERR_INVALID_VALUE;
+  if (!in_scales || !(n_in_scales == 1 || n_in_scales == cext)) return QNN_ERR_INVALID_VALUE;
+  if (n_in_scales > kMaxChanParams) return QNN_ERR_UNSUPPORTED;
+  if (!scale_ok(out_scale)) return QNN_ERR_INVALID_VALUE;
+  if (count > 0 && (!in || !out)) return QNN_ERR_INVALID_VALUE;
+  for (int c = 0; c < n_in_scales; ++c) {
+    if (!scale_ok(in_scales[c])) return QNN_ERR_INVALID_VALUE;
+    int32_t M, r;
+    if (!kernel_multiplier((double)in_scales[c] / (double)out_scale, &M, &r)) return QNN_ERR_UNSUPPORTED;
+    p.mult[c] = M;
+    p.rsh[c] = (int8_t)r;
+  }
+  if (count == 0) return QNN_OK;
+  p.in = in;
+  p.out = out;
+  p.count = count;
+  p.inner = inner;
+  p.cext = cext;
+  p.nch = n_in_scales;
+  p.in_dt = (int)in_dtype;
+  p.out_dt = (int)out_dtype;
+  p.mode = (int)rounding;
+  p.in_zp = in_zp;
+  p.out_zp = out_zp;
+  p.lo = (int32_t)lo;
+  p.hi = (int32_t)hi;
+  return cuda_status(launch_requantize(p, (cudaStream_t)stream));
+}
+
+static qnn_status_t quant_common(const void* in, void* out, qnn_dtype_t qdt, const int64_t* shape, int32_t ndim,
+                                 int32_t axis, const float* scales, const int32_t* zps, int32_t n, bool quantize,
+                                 cudaStream_t stream) {
+  static QuantParams p;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  long long count, inner;
+  int cext;
+  qnn_status_t st = shape_info(shape, ndim, axis, &count, &inner, &cext);
+  if (st != QNN_OK) return st;
+  int64_t lo, hi;
+  if (!dtype_range(qdt, &lo, &hi)) return QNN_ERR_UNSUPPORTED;
+  if (quantize && !is_8bit(qdt)) return QNN_ERR_UNSUPPORTED;
+  if (!scales || !zps || !(n == 1 || n == cext)) return QNN_ERR_INVALID_VALUE;
+  if (n > kMaxQuantParams) return QNN_ERR_UNSUPPORTED;
+  for (int c = 0; c < n; ++c) {
+    if (!scale_ok(scales[c]) || !zp_ok(qdt, zps[c])) return QNN_ERR_INVALID_VALUE;
+    p.scale[c] = scales[c];
+    p.zp[c] = zps[c];
+  }
+  if (count > 0 && (!in || !out)) return QNN_ERR_INVALID_VALUE;
+  if (count == 0) return QNN_OK;
+  p.in = in;
+  p.out = out;
+  p.count = count;
+  p.inner = inner;
+  p.cext = cext;
+  p.nch = n;
+  p.q_dt = (int)qdt;
+  p.lo = (int32_t)lo;
+  p.hi = (int32_t)hi;
+  return cuda_status(quantize ? launch_quantize(p, stream) : launch_dequantize(p, stream));
+}
+
+qnn_status_t qnn_quantize(const float* in, void* out, qnn_dtype_t out_dtype, const int64_t* shape, int32_t ndim,
+                          int32_t axis, const float* scales, const int32_t* zero_points, int32_t n_params,
+                          qnn_stream_t stream) {
+  return quant_common(in, out, out_dtype, shape, ndim, axis, scales, zero_points, n_params, true,
+                      (cudaStream_t)stream);
+}
+
+qnn_status_t qnn_dequantize(const void* in, qnn_dtype_t in_dtype, float* out, const int64_t* shape, int32_t ndim,
+                            int32_t axis, const float* scales, const int32_t* zero_points, int32_t n_params,
+                            qnn_stream_t stream) {
+  return quant_common(in, out, in_dtype, shape, ndim, axis, scales, zero_points, n_params, false,
+                      (cudaStream_t)stream);
+}
+
+}  // extern "C"

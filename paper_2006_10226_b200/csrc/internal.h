@@ -1,0 +1,131 @@
+// internal.h — parameter blocks and launcher declarations shared by the host
+// ABI (abi.cu) and the kernel translation units.  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace qnn {
+
+constexpr int kMaxChanParams = 4096;   // per-channel requantize multipliers in kernel params
+constexpr int kMaxQuantParams = 2048;  // per-channel quantize/dequantize params in kernel params
+
+// ---------------------------------------------------------------------------
+// Tensor-core implicit-GEMM conv / dense (gemm_sm100.cu)
+//   rows m  = output pixels (n, p, q) in NHWC order,   M = N*P*Q
+//   cols k  = output channels,                          Nout = K
+//   reduce  = (r, s, c-chunk) k-blocks of BK bytes,     num_kb = R*S*nchunks
+// ---------------------------------------------------------------------------
+struct GemmEpilogue {
+  const int32_t* off;      // [ncls][Kpad]: bias - zpA*colsum_cls + zpA*zpW*Cg*nvalid_cls
+  const int32_t* mult;     // [Kpad] fixed-point multiplier M_k
+  const int32_t* rsh;      // [Kpad] right shift 31 - shift_k (1..62)
+  const uint8_t* rowcls;   // [P] row border class (nullptr => class 0)
+  const uint8_t* colcls;   // [Q] column border class
+  const int32_t* rowsum;   // [M] Term-3 row sums (nullptr when zp_W == 0)
+  void* out;
+  long long out_pitch;     // elements between consecutive output pixels
+  int ncc;                 // number of column classes
+  int Kpad;
+  int32_t zpW;
+  int out_dtype;           // DT_U8 / DT_S8 / DT_S32
+  int requant;             // 0 => raw int32 (Eq. 3 + bias)
+  int mode;                // rounding
+  int32_t zp_out, lo, hi;  // lo/hi already include ReLU, act clamp and dtype range
+};
+
+struct GemmParams {
+  int M, Nout;
+  int num_kb, nchunks, S, dil_h, dil_w;
+  int BK, BN, stages;
+  int num_m_tiles, num_n_tiles;
+  int im2col;              // 1 => A via im2col TMA over NHWC, 0 => A is a 2-D [M][C] matrix
+  int P, Q, sh, sw, pt, pl;
+  uint32_t idesc;
+  GemmEpilogue e;
+};
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmEpiWarps = 8;
+constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
+
+size_t gemm_smem_bytes(int BK, int BN, int stages);
+int gemm_max_stages(int BK, int BN);
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p, int grid,
+                        cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// Prepack / auxiliary kernels (prep.cu)
+// ---------------------------------------------------------------------------
+struct ClassTable {
+  int ncr, ncc;
+  int r_lo[32], r_hi[32];  // valid filter-row range per row class
+  int s_lo[32], s_hi[32];  // valid filter-col range per col class
+};
+
+cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad,
+                                cudaStream_t s);
+cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
+                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int Kpad,
+                                cudaStream_t s);
+cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int16_t* Wd, int C, int RS,
+                                   cudaStream_t s);
+cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out, int Cp, long long npix, int C,
+                                cudaStream_t s);
+cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
+                              int32_t* pixsum, cudaStream_t s);
+cudaError_t launch_window_sums(const int32_t* pixsum, int N, int H, int W, int P, int Q, int R, int S, int sh,
+                               int sw, int pt, int pl, int dh, int dw, int32_t* rowsum, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Depthwise conv (depthwise.cu): subtract-first lowering on CUDA cores
+// ---------------------------------------------------------------------------
+struct DwParams {
+  const void* in;
+  const int16_t* w;        // [R*S][C] holding W - zp_W
+  const int32_t* bias;     // [C] or nullptr
+  const int32_t* mult;     // [C]
+  const int32_t* rsh;      // [C]
+  void* out;
+  long long in_cstride, out_cstride;
+  int N, H, W, C, P, Q, R, S, sh, sw, pt, pl, dh, dw;
+  int a_signed;
+  int32_t zpA;
+  int out_dtype, requant, mode;
+  int32_t zp_out, lo, hi;
+};
+cudaError_t launch_depthwise(const DwParams& p, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Elementwise (elementwise.cu)
+// ---------------------------------------------------------------------------
+struct RequantParams {
+  const void* in;
+  void* out;
+  long long count, inner;
+  int cext, nch;
+  int in_dt, out_dt, mode;
+  int32_t in_zp, out_zp, lo, hi;
+  int32_t mult[kMaxChanParams];
+  int8_t rsh[kMaxChanParams];
+};
+struct QuantParams {
+  const void* in;
+  void* out;
+  long long count, inner;
+  int cext, nch;
+  int q_dt;               // quantized dtype (out of quantize / in of dequantize)
+  int32_t lo, hi;
+  float scale[kMaxQuantParams];
+  int32_t zp[kMaxQuantParams];
+};
+cudaError_t launch_requantize(const RequantParams& p, cudaStream_t s);
+cudaError_t launch_quantize(const QuantParams& p, cudaStream_t s);
+cudaError_t launch_dequantize(const QuantParams& p, cudaStream_t s);
+
+// launch accounting (abi.cu)
+void count_launch(int n = 1);
+
+}  // namespace qnn

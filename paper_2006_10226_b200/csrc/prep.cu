@@ -1,0 +1,188 @@
+// prep.cu — compile-time folding (weight prepack) and the auxiliary kernels of
+// the conv path.
+//
+//  * pack_weights   : OHWI weights -> [Kpad][R*S][Cw] zero-padded, the B operand
+//                     of the implicit GEMM (pad channels/rows are 0: reading R8).
+//  * fold_offsets   : "term 2 and term 4 are compile-time constants" (P:259,
+//                     P:264).  Per border class cls and channel k:
+//                       off = bias[k] - zp_A * sum_{valid taps, c} W[k,r,s,c]
+//                                     + zp_A * zp_W * C * nvalid_taps(cls)
+//                     which also restores the zero-point padding that
+//                     TMA's zero fill omits (reading R7).
+//  * pixel_sums / window_sums : Term 3 ("sliding window reduction ... pool2d,
+//                     reduce sum"): rowsum[n,p,q] = sum over valid taps
+//                     of sum_c A.  Only launched when zp_W != 0.
+//  * pad_channels   : copies an input whose pixel pitch is not a multiple of 16
+//                     bytes into a zero-padded pitch the TMA can address.
+#include "common.cuh"
+#include "internal.h"
+
+namespace qnn {
+
+__global__ void pack_weights_kernel(const uint8_t* __restrict__ W, uint8_t* __restrict__ Wp, int K, int RS, int C,
+                                    int Cw, int Kpad) {
+  const long long total = (long long)Kpad * RS * Cw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cw);
+    const long long t = i / Cw;
+    const int tap = (int)(t % RS);
+    const int k = (int)(t / RS);
+    uint8_t v = 0;
+    if (k < K && c < C) v = W[((long long)k * RS + tap) * C + c];
+    Wp[i] = v;
+  }
+}
+
+cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad, cudaStream_t s) {
+  const long long total = (long long)Kpad * RS * Cw;
+  const int threads = 256;
+  const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 4096);
+  pack_weights_kernel<<<blocks, threads, 0, s>>>((const uint8_t*)W, (uint8_t*)Wp, K, RS, C, Cw, Kpad);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed, const int32_t* __restrict__ bias,
+                                    int K, int R, int S, int C, int32_t zpA, int32_t zpW, ClassTable ct,
+                                    int32_t* __restrict__ off, int Kpad) {
+  const int ncls = ct.ncr * ct.ncc;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ncls * Kpad) return;
+  const int cls = idx / Kpad, k = idx - cls * Kpad;
+  if (k >= K) {
+    off[idx] = 0;
+    return;
+  }
+  const int rc = cls / ct.ncc, cc = cls - rc * ct.ncc;
+  const int r0 = ct.r_lo[rc], r1 = ct.r_hi[rc], s0 = ct.s_lo[cc], s1 = ct.s_hi[cc];
+  long long colsum = 0;
+  int nvalid = 0;
+  for (int r = r0; r <= r1; ++r)
+    for (int s = s0; s <= s1; ++s) {
+      ++nvalid;
+      const uint8_t* w = W + (((long long)k * R + r) * S + s) * C;
+      for (int c = 0; c < C; ++c) colsum += w_signed ? (long long)(int8_t)w[c] : (long long)w[c];
+    }
+  // int32 wrap is exact for the final sum (reading R10); compute in 64-bit then wrap.
+  const long long v = (bias ? (long long)bias[k] : 0) - (long long)zpA * colsum +
+                      (long long)zpA * zpW * (long long)C * nvalid;
+  off[idx] = (int32_t)(uint32_t)(unsigned long long)v;
+}
+
+cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
+                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int Kpad,
+                                cudaStream_t s) {
+  const int total = ct.ncr * ct.ncc * Kpad;
+  fold_offsets_kernel<<<(total + 127) / 128, 128, 0, s>>>((const uint8_t*)W, w_signed, bias, K, R, S, C, zpA, zpW,
+                                                         ct, off, Kpad);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// depthwise weights K x R x S x 1 (K == C) -> [R*S][C] int16 holding W - zp_W
+__global__ void pack_dw_weights_kernel(const uint8_t* __restrict__ W, int w_signed, int32_t zpW,
+                                       int16_t* __restrict__ Wd, int C, int RS) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C * RS) return;
+  const int tap = i / C, c = i - tap * C;
+  const uint8_t b = W[(long long)c * RS + tap];
+  const int v = w_signed ? (int)(int8_t)b : (int)b;
+  Wd[i] = (int16_t)(v - zpW);
+}
+
+cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int16_t* Wd, int C, int RS,
+                                   cudaStream_t s) {
+  pack_dw_weights_kernel<<<(C * RS + 255) / 256, 256, 0, s>>>((const uint8_t*)W, w_signed, zpW, Wd, C, RS);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void pad_channels_kernel(const uint8_t* __restrict__ in, long long in_cstride, uint8_t* __restrict__ out,
+                                    int Cp, long long npix, int C) {
+  const long long total = npix * Cp;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pix = i / Cp;
+    const int c = (int)(i - pix * Cp);
+    out[i] = c < C ? in[pix * in_cstride + c] : (uint8_t)0;
+  }
+}
+
+cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out, int Cp, long long npix, int C,
+                                cudaStream_t s) {
+  const long long total = npix * Cp;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  pad_channels_kernel<<<blocks, 256, 0, s>>>((const uint8_t*)in, in_cstride, (uint8_t*)out, Cp, npix, C);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Term 3, step 1: per-pixel channel sums (one warp-cooperative pass over A).
+__global__ void pixel_sums_kernel(const uint8_t* __restrict__ in, int a_signed, long long in_cstride, int C,
+                                  long long npix, int32_t* __restrict__ pixsum) {
+  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (pix >= npix) return;
+  const uint8_t* a = in + pix * in_cstride;
+  int32_t s = 0;
+  int c = 0;
+  if ((in_cstride & 15) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    for (; c + 16 <= C; c += 16) {
+      const uint4 v = *reinterpret_cast<const uint4*>(a + c);
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (a_signed)
+          s = __dp4a((int)w4[j], 0x01010101, s);
+        else
+          s = (int32_t)__dp4a(w4[j], 0x01010101u, (uint32_t)s);
+      }
+    }
+  }
+  for (; c < C; ++c) s += a_signed ? (int32_t)(int8_t)a[c] : (int32_t)a[c];
+  pixsum[pix] = s;
+}
+
+cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
+                              int32_t* pixsum, cudaStream_t s) {
+  pixel_sums_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride, C,
+                                                                    npix, pixsum);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Term 3, step 2: rowsum[n,p,q] = sum over in-image taps (r,s) of pixsum
+// (zero-filled taps contribute 0; their zp part lives in the class offsets).
+__global__ void window_sums_kernel(const int32_t* __restrict__ pixsum, int N, int H, int W, int P, int Q, int R,
+                                   int S, int sh, int sw, int pt, int pl, int dh, int dw,
+                                   int32_t* __restrict__ rowsum) {
+  const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long M = (long long)N * P * Q;
+  if (m >= M) return;
+  const int q = (int)(m % Q);
+  const long long t = m / Q;
+  const int p = (int)(t % P);
+  const int n = (int)(t / P);
+  int32_t s = 0;
+  for (int r = 0; r < R; ++r) {
+    const int h = p * sh + r * dh - pt;
+    if (h < 0 || h >= H) continue;
+    for (int c = 0; c < S; ++c) {
+      const int w = q * sw + c * dw - pl;
+      if (w < 0 || w >= W) continue;
+      s += pixsum[((long long)n * H + h) * W + w];
+    }
+  }
+  rowsum[m] = s;
+}
+
+cudaError_t launch_window_sums(const int32_t* pixsum, int N, int H, int W, int P, int Q, int R, int S, int sh,
+                               int sw, int pt, int pl, int dh, int dw, int32_t* rowsum, cudaStream_t s) {
+  const long long M = (long long)N * P * Q;
+  window_sums_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(pixsum, N, H, W, P, Q, R, S, sh, sw, pt, pl, dh,
+                                                                  dw, rowsum);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace qnn

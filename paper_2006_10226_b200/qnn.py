@@ -1,0 +1,326 @@
+"""Thin Python binding of libqnn.so (include/qnn.h) — argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind the C ABI; PyTorch only
+provides device memory (``data_ptr()``) and the current CUDA stream.  There is
+no CPU fallback: if ``libqnn.so`` is missing or a call fails, an exception is
+raised.  Function names mirror the C entry points.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Sequence
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libqnn.so")
+_lock = threading.Lock()
+_lib = None
+
+QNN_S8, QNN_U8, QNN_S32, QNN_F32 = 0, 1, 2, 3
+ROUNDING = {"upward": 0, "tonearest": 1}
+STATUS = {0: "QNN_OK", 1: "QNN_ERR_INVALID_VALUE", 2: "QNN_ERR_UNSUPPORTED", 3: "QNN_ERR_MISALIGNED",
+          4: "QNN_ERR_WORKSPACE", 5: "QNN_ERR_CUDA"}
+_TORCH_DT = {torch.int8: QNN_S8, torch.uint8: QNN_U8, torch.int32: QNN_S32, torch.float32: QNN_F32}
+_DT_TORCH = {v: k for k, v in _TORCH_DT.items()}
+_NAME_DT = {"s8": QNN_S8, "u8": QNN_U8, "s32": QNN_S32, "f32": QNN_F32}
+INT32_MIN, INT32_MAX = -(2 ** 31), 2 ** 31 - 1
+
+EXPORTED = ["qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset", "qnn_derive_multiplier",
+            "qnn_conv2d_prepack_size", "qnn_conv2d_prepack", "qnn_conv2d_workspace_size", "qnn_conv2d_packed",
+            "qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense_prepack_size", "qnn_dense_prepack",
+            "qnn_dense_workspace_size", "qnn_dense_packed", "qnn_dense", "qnn_requantize", "qnn_quantize",
+            "qnn_dequantize"]
+
+
+class QnnError(RuntimeError):
+    pass
+
+
+class OutputParams(ctypes.Structure):
+    _fields_ = [("output_scale", ctypes.c_float), ("output_zero_point", ctypes.c_int32),
+                ("out_dtype", ctypes.c_int), ("rounding", ctypes.c_int), ("relu", ctypes.c_int32),
+                ("act_min", ctypes.c_int32), ("act_max", ctypes.c_int32)]
+
+
+class Conv2dDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("N", "H", "W", "C", "K", "R", "S", "stride_h", "stride_w", "pad_t", "pad_l", "pad_b", "pad_r",
+                 "dil_h", "dil_w", "groups", "in_cstride", "out_cstride")] + [
+        ("input_dtype", ctypes.c_int), ("kernel_dtype", ctypes.c_int),
+        ("input_zero_point", ctypes.c_int32), ("kernel_zero_point", ctypes.c_int32),
+        ("input_scale", ctypes.c_float), ("kernel_scales", ctypes.POINTER(ctypes.c_float)),
+        ("num_kernel_scales", ctypes.c_int32)]
+
+
+class DenseDesc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("lda", ctypes.c_int32),
+                ("ldc", ctypes.c_int32), ("a_dtype", ctypes.c_int), ("w_dtype", ctypes.c_int),
+                ("zp_A", ctypes.c_int32), ("zp_W", ctypes.c_int32), ("s_A", ctypes.c_float),
+                ("s_W", ctypes.POINTER(ctypes.c_float)), ("n_sW", ctypes.c_int32)]
+
+
+def lib() -> ctypes.CDLL:
+    """Load libqnn.so (raises if it has not been built: no fallback path exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                if os.environ.get("QNN_AUTOBUILD"):
+                    from . import build as _b
+                    _b.build()
+                else:
+                    raise QnnError(f"{LIB_PATH} not built; run `python -m paper_2006_10226_b200.build`")
+            L = ctypes.CDLL(LIB_PATH)
+            vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+            cdp, odp, ddp = ctypes.POINTER(Conv2dDesc), ctypes.POINTER(OutputParams), ctypes.POINTER(DenseDesc)
+            L.qnn_status_string.restype = ctypes.c_char_p
+            L.qnn_launch_counter.restype = ctypes.c_uint64
+            L.qnn_derive_multiplier.argtypes = [ctypes.c_double, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+            L.qnn_conv2d_prepack_size.argtypes = [cdp, odp, ctypes.POINTER(sz)]
+            L.qnn_conv2d_prepack.argtypes = [cdp, vp, vp, odp, vp, sz, vp]
+            L.qnn_conv2d_workspace_size.argtypes = [cdp, odp, ctypes.POINTER(sz)]
+            L.qnn_conv2d_packed.argtypes = [cdp, odp, vp, vp, vp, vp, sz, vp]
+            L.qnn_conv2d.argtypes = [cdp, vp, vp, vp, odp, vp, vp, sz, vp]
+            L.qnn_depthwise_conv2d.argtypes = [cdp, vp, vp, vp, odp, vp, vp, sz, vp]
+            L.qnn_dense_prepack_size.argtypes = [ddp, odp, ctypes.POINTER(sz)]
+            L.qnn_dense_prepack.argtypes = [ddp, vp, vp, odp, vp, sz, vp]
+            L.qnn_dense_workspace_size.argtypes = [ddp, odp, ctypes.POINTER(sz)]
+            L.qnn_dense_packed.argtypes = [ddp, odp, vp, vp, vp, vp, sz, vp]
+            L.qnn_dense.argtypes = [ddp, vp, vp, vp, odp, vp, vp, sz, vp]
+            L.qnn_requantize.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.POINTER(i64), i32, i32,
+                                         ctypes.POINTER(ctypes.c_float), i32, i32, ctypes.c_float, i32,
+                                         ctypes.c_int, vp]
+            L.qnn_quantize.argtypes = [vp, vp, ctypes.c_int, ctypes.POINTER(i64), i32, i32,
+                                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
+            L.qnn_dequantize.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(i64), i32, i32,
+                                         ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
+            for name in EXPORTED:
+                if name not in ("qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset"):
+                    getattr(L, name).restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise QnnError(f"{what}: {STATUS.get(status, status)}")
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise QnnError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise QnnError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _floats(v) -> ctypes.Array:
+    vals = [float(x) for x in (v.tolist() if hasattr(v, "tolist") else (v if isinstance(v, Sequence) else [v]))]
+    return (ctypes.c_float * len(vals))(*vals)
+
+
+def _ints(v) -> ctypes.Array:
+    vals = [int(x) for x in (v.tolist() if hasattr(v, "tolist") else (v if isinstance(v, Sequence) else [v]))]
+    return (ctypes.c_int32 * len(vals))(*vals)
+
+
+def _dtcode(dt) -> int:
+    if isinstance(dt, str):
+        return _NAME_DT[dt]
+    return _TORCH_DT[dt]
+
+
+def launch_counter() -> int:
+    return int(lib().qnn_launch_counter())
+
+
+def launch_counter_reset():
+    lib().qnn_launch_counter_reset()
+
+
+def qnn_derive_multiplier(m: float) -> tuple[int, int]:
+    M, s = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().qnn_derive_multiplier(float(m), ctypes.byref(M), ctypes.byref(s)), "qnn_derive_multiplier")
+    return M.value, s.value
+
+
+def output_params(scale: float, zero_point: int, dtype="u8", rounding="upward", relu=False, act_min=None,
+                  act_max=None) -> OutputParams:
+    return OutputParams(float(scale), int(zero_point), _dtcode(dtype), ROUNDING[rounding], int(bool(relu)),
+                        INT32_MIN if act_min is None else int(act_min), INT32_MAX if act_max is None else int(act_max))
+
+
+# --------------------------------------------------------------------------- conv2d / depthwise
+class PackedConv2d:
+    """qnn.conv2d with its compile-time folding done once.
+
+    ``x`` NHWC (u8/s8), ``w`` OHWI (K,R,S,C/groups) on the GPU, ``bias`` int32[K] or None.
+    ``out`` None -> raw int32 Eq. 3 result (+bias); else a dict (scale, zero_point, dtype,
+    rounding, relu, act_min, act_max) for the fused requantize epilogue.
+    """
+
+    def __init__(self, N, H, W, C, w: torch.Tensor, bias: torch.Tensor | None, zp_A: int, zp_W: int, s_A: float,
+                 s_W, out: dict | None = None, stride=(1, 1), pad=(0, 0, 0, 0), dil=(1, 1), groups=1,
+                 input_dtype="u8", in_cstride=0, out_cstride=0, stream=None):
+        K, R, S, Cg = w.shape
+        self._scales = _floats(s_W)
+        d = Conv2dDesc()
+        for k, v in dict(N=N, H=H, W=W, C=C, K=K, R=R, S=S, stride_h=stride[0], stride_w=stride[1], pad_t=pad[0],
+                         pad_l=pad[1], pad_b=pad[2], pad_r=pad[3], dil_h=dil[0], dil_w=dil[1], groups=groups,
+                         in_cstride=in_cstride, out_cstride=out_cstride).items():
+            setattr(d, k, int(v))
+        d.input_dtype = _dtcode(input_dtype)
+        d.kernel_dtype = _dtcode(w.dtype)
+        d.input_zero_point = int(zp_A)
+        d.kernel_zero_point = int(zp_W)
+        d.input_scale = float(s_A)
+        d.kernel_scales = ctypes.cast(self._scales, ctypes.POINTER(ctypes.c_float))
+        d.num_kernel_scales = len(self._scales)
+        self.desc = d
+        self.out = out
+        self.o = output_params(**out) if out is not None else None
+        self._op = ctypes.byref(self.o) if self.o is not None else None
+        self.P = (H + pad[0] + pad[2] - dil[0] * (R - 1) - 1) // stride[0] + 1
+        self.Q = (W + pad[1] + pad[3] - dil[1] * (S - 1) - 1) // stride[1] + 1
+        self.K = K
+        self.out_dtype = _DT_TORCH[self.o.out_dtype] if self.o is not None else torch.int32
+        L = lib()
+        n = ctypes.c_size_t()
+        _check(L.qnn_conv2d_prepack_size(ctypes.byref(d), self._op, ctypes.byref(n)), "qnn_conv2d_prepack_size")
+        dev = w.device
+        self.packed = torch.empty(max(n.value, 256), dtype=torch.uint8, device=dev)
+        _check(L.qnn_conv2d_prepack(ctypes.byref(d), _dev(w, "w"), None if bias is None else _dev(bias, "bias"),
+                                    self._op, ctypes.c_void_p(self.packed.data_ptr()), n.value,
+                                    ctypes.c_void_p(_stream(stream))), "qnn_conv2d_prepack")
+        _check(L.qnn_conv2d_workspace_size(ctypes.byref(d), self._op, ctypes.byref(n)), "qnn_conv2d_workspace_size")
+        self.ws_bytes = n.value
+        self.workspace = torch.empty(max(n.value, 256), dtype=torch.uint8, device=dev) if n.value else None
+
+    def out_shape(self):
+        d = self.desc
+        return (d.N, self.P, self.Q, d.out_cstride or self.K)
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(self.out_shape(), dtype=self.out_dtype, device=x.device)
+        ws = ctypes.c_void_p(self.workspace.data_ptr()) if self.workspace is not None else None
+        _check(lib().qnn_conv2d_packed(ctypes.byref(self.desc), self._op, ctypes.c_void_p(self.packed.data_ptr()),
+                                       _dev(x, "x"), _dev(out, "out"), ws, self.ws_bytes,
+                                       ctypes.c_void_p(_stream(stream))), "qnn_conv2d_packed")
+        return out
+
+
+def qnn_conv2d(x: torch.Tensor, w: torch.Tensor, bias, zp_A, zp_W, s_A, s_W, out: dict | None = None,
+               stride=(1, 1), pad=(0, 0, 0, 0), dil=(1, 1), groups=1) -> torch.Tensor:
+    """One-shot qnn.conv2d (prepack + run) on NHWC x / OHWI w."""
+    N, H, W, C = x.shape
+    op = PackedConv2d(N, H, W, C, w, bias, zp_A, zp_W, s_A, s_W, out, stride, pad, dil, groups,
+                      input_dtype="s8" if x.dtype == torch.int8 else "u8")
+    return op(x)
+
+
+def qnn_depthwise_conv2d(x, w, bias, zp_A, zp_W, s_A, s_W, out=None, stride=(1, 1), pad=(0, 0, 0, 0), dil=(1, 1)):
+    C = x.shape[3]
+    return qnn_conv2d(x, w, bias, zp_A, zp_W, s_A, s_W, out, stride, pad, dil, groups=C)
+
+
+# --------------------------------------------------------------------------- dense
+class PackedDense:
+    """qnn.dense: out[m, n] over A (M x K) and W (N x K) with folded constants."""
+
+    def __init__(self, M, w: torch.Tensor, bias, zp_A, zp_W, s_A, s_W, out: dict | None = None, a_dtype="u8",
+                 stream=None):
+        N, K = w.shape
+        self._scales = _floats(s_W)
+        d = DenseDesc()
+        d.M, d.N, d.K, d.lda, d.ldc = int(M), int(N), int(K), 0, 0
+        d.a_dtype = _dtcode(a_dtype)
+        d.w_dtype = _dtcode(w.dtype)
+        d.zp_A, d.zp_W, d.s_A = int(zp_A), int(zp_W), float(s_A)
+        d.s_W = ctypes.cast(self._scales, ctypes.POINTER(ctypes.c_float))
+        d.n_sW = len(self._scales)
+        self.desc = d
+        self.o = output_params(**out) if out is not None else None
+        self._op = ctypes.byref(self.o) if self.o is not None else None
+        self.out_dtype = _DT_TORCH[self.o.out_dtype] if self.o is not None else torch.int32
+        L = lib()
+        n = ctypes.c_size_t()
+        _check(L.qnn_dense_prepack_size(ctypes.byref(d), self._op, ctypes.byref(n)), "qnn_dense_prepack_size")
+        self.packed = torch.empty(max(n.value, 256), dtype=torch.uint8, device=w.device)
+        _check(L.qnn_dense_prepack(ctypes.byref(d), _dev(w, "w"), None if bias is None else _dev(bias, "bias"),
+                                   self._op, ctypes.c_void_p(self.packed.data_ptr()), n.value,
+                                   ctypes.c_void_p(_stream(stream))), "qnn_dense_prepack")
+        _check(L.qnn_dense_workspace_size(ctypes.byref(d), self._op, ctypes.byref(n)), "qnn_dense_workspace_size")
+        self.ws_bytes = n.value
+        self.workspace = torch.empty(max(n.value, 256), dtype=torch.uint8, device=w.device) if n.value else None
+
+    def __call__(self, a: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self.desc.M, self.desc.N), dtype=self.out_dtype, device=a.device)
+        ws = ctypes.c_void_p(self.workspace.data_ptr()) if self.workspace is not None else None
+        _check(lib().qnn_dense_packed(ctypes.byref(self.desc), self._op, ctypes.c_void_p(self.packed.data_ptr()),
+                                      _dev(a, "a"), _dev(out, "out"), ws, self.ws_bytes,
+                                      ctypes.c_void_p(_stream(stream))), "qnn_dense_packed")
+        return out
+
+
+def qnn_dense(a: torch.Tensor, w: torch.Tensor, bias, zp_A, zp_W, s_A, s_W, out: dict | None = None):
+    op = PackedDense(a.shape[0], w, bias, zp_A, zp_W, s_A, s_W, out, a_dtype="s8" if a.dtype == torch.int8 else "u8")
+    return op(a)
+
+
+# --------------------------------------------------------------------------- elementwise
+def _shape(t: torch.Tensor):
+    shp = list(t.shape) or [1]
+    return (ctypes.c_int64 * len(shp))(*shp), len(shp)
+
+
+def qnn_requantize(x: torch.Tensor, in_scales, in_zp: int, out_scale: float, out_zp: int, out_dtype="u8",
+                   rounding="upward", axis=-1, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    odt = _dtcode(out_dtype)
+    if out is None:
+        out = torch.empty(x.shape, dtype=_DT_TORCH[odt], device=x.device)
+    shp, nd = _shape(x)
+    sc = _floats(in_scales)
+    _check(lib().qnn_requantize(_dev(x, "x"), _TORCH_DT[x.dtype], _dev(out, "out"), odt, shp, nd, int(axis), sc,
+                                len(sc), int(in_zp), float(out_scale), int(out_zp), ROUNDING[rounding],
+                                ctypes.c_void_p(_stream(stream))), "qnn_requantize")
+    return out
+
+
+def qnn_quantize(x: torch.Tensor, scales, zero_points, out_dtype="u8", axis=-1, out=None, stream=None):
+    odt = _dtcode(out_dtype)
+    if out is None:
+        out = torch.empty(x.shape, dtype=_DT_TORCH[odt], device=x.device)
+    shp, nd = _shape(x)
+    sc, zp = _floats(scales), _ints(zero_points)
+    if len(zp) == 1 and len(sc) > 1:
+        zp = _ints([zp[0]] * len(sc))
+    if len(sc) == 1 and len(zp) > 1:
+        sc = _floats([sc[0]] * len(zp))
+    _check(lib().qnn_quantize(_dev(x, "x"), _dev(out, "out"), odt, shp, nd, int(axis), sc, zp, len(sc),
+                              ctypes.c_void_p(_stream(stream))), "qnn_quantize")
+    return out
+
+
+def qnn_dequantize(q: torch.Tensor, scales, zero_points, axis=-1, out=None, stream=None):
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    shp, nd = _shape(q)
+    sc, zp = _floats(scales), _ints(zero_points)
+    if len(zp) == 1 and len(sc) > 1:
+        zp = _ints([zp[0]] * len(sc))
+    if len(sc) == 1 and len(zp) > 1:
+        sc = _floats([sc[0]] * len(zp))
+    _check(lib().qnn_dequantize(_dev(q, "q"), _TORCH_DT[q.dtype], _dev(out, "out"), shp, nd, int(axis), sc, zp,
+                                len(sc), ctypes.c_void_p(_stream(stream))), "qnn_dequantize")
+    return out

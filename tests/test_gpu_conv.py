@@ -1,0 +1,176 @@
+"""GPU parity: qnn.conv2d (tcgen05 implicit GEMM + fused epilogue) and the
+depthwise kernel vs the oracle, bit-exact, on seeded inputs.
+
+Coverage: BASELINE config 1 (both outputs, both rounding modes, pad 0/1);
+random shapes spanning several 128-row tiles with ragged tails, strides,
+dilation, asymmetric padding, u8/s8 operands, zp_W != 0 (Term 3 row sums),
+channel counts that need the padded-pitch copy, K not a multiple of 32,
+multiple N tiles, raw int32 output, a channel-strided output; ResNet-50 and
+MobileNet-v2 layer shapes (full compare at batch 1, sampled at batch 64/128).
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from gpu_helpers import gpu_conv, mismatch_report, oracle_conv, oracle_conv_at
+from workloads import gen
+from workloads.shapes import mobilenet_v2_convs, resnet50_unique
+
+pytestmark = pytest.mark.gpu
+
+
+def config1_case(pad, relu, mode):
+    """BASELINE.json configs[0]: N=1, C=16, H=W=8, K=16, 3x3, u8 input zp=128,
+    s8 per-channel weights, requantize to u8 (reading R18 for the unstated details)."""
+    g = np.random.default_rng(101)
+    A = gen.rand_q(g, (1, 8, 8, 16), "u8")
+    W = gen.rand_q(np.random.default_rng(102), (16, 3, 3, 16), "s8", -127, 127)
+    k = np.arange(16)
+    s_W = np.where(k < 8, 2.0 ** -7 * 2.0 ** -(k % 4), 0.0037 * (1 + k / 16)).astype(np.float32)
+    bias = np.random.default_rng(103).integers(-4096, 4097, size=16).astype(np.int32)
+    return gen.ConvCase(A, W, bias, 128, 0, 0.5, s_W, 4.0, 0 if relu else 128, "u8", (1, 1), (pad,) * 4, (1, 1), 1,
+                        relu, None, None, mode)
+
+
+@pytest.mark.parametrize("pad", [1, 0])
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("mode", ["upward", "tonearest"])
+def test_config1(pad, relu, mode):
+    case = config1_case(pad, relu, mode)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+SWEEP = [
+    # N, C, H, W, K, R, S, stride, pad(t,l,b,r), dil, a, w, zpW, out, per_channel
+    (2, 16, 9, 11, 16, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "s8", 0, "u8", True),
+    (3, 64, 20, 19, 64, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "s8", 0, "u8", True),
+    (2, 64, 17, 17, 96, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 0, "s8", True),
+    (2, 128, 15, 15, 256, 1, 1, (2, 2), (0, 0, 0, 0), (1, 1), "u8", "s8", 0, "u8", True),
+    (1, 32, 23, 21, 48, 5, 5, (1, 1), (2, 2, 2, 2), (1, 1), "u8", "s8", 0, "u8", True),
+    (2, 48, 13, 14, 64, 3, 3, (2, 2), (1, 1, 1, 1), (1, 1), "s8", "s8", 0, "s8", True),
+    (2, 32, 12, 12, 40, 3, 3, (1, 1), (2, 2, 2, 2), (2, 2), "u8", "s8", 0, "u8", True),
+    (1, 80, 10, 17, 100, 1, 7, (1, 1), (0, 3, 0, 3), (1, 1), "u8", "s8", 0, "u8", True),
+    (1, 80, 17, 10, 100, 7, 1, (1, 1), (3, 0, 3, 0), (1, 1), "u8", "s8", 0, "u8", True),
+    (2, 64, 11, 9, 64, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "u8", 117, "u8", False),   # TFLite u8 x u8
+    (2, 96, 14, 14, 300, 3, 3, (2, 2), (0, 1, 1, 0), (1, 1), "u8", "u8", 131, "u8", False),  # asym pad, 2 N tiles
+    (1, 3, 30, 30, 32, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0, "u8", True),     # stem: pad-copy
+    (2, 24, 16, 16, 72, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 0, "u8", True),    # C=24: pad-copy, 2-D A
+    (1, 144, 9, 9, 24, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "s8", "s8", -7, "s8", True),
+    (2, 256, 7, 7, 512, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "s8", 0, "u8", True),
+    (1, 64, 8, 8, 1000, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 0, "u8", True),    # K=1000 tail
+    (2, 32, 10, 10, 64, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "s8", 0, "s32", True),   # raw int32
+    (1, 16, 5, 5, 16, 5, 5, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 3, "s32", True),     # 1x1 output, raw
+]
+
+
+@pytest.mark.parametrize("i", range(len(SWEEP)))
+def test_conv_sweep(i):
+    N, C, H, W, K, R, S, st, pad, dil, adt, wdt, zpW, odt, pc = SWEEP[i]
+    for mode in ("upward", "tonearest"):
+        case = gen.conv_case(500 + i, N, C, H, W, K, R, S, st, pad, dil, 1, adt, wdt, zp_W=zpW, per_channel=pc,
+                             out_dtype=odt, relu=(i % 2 == 0), rounding=mode)
+        _, _, y = gpu_conv(case)
+        got, want = y.cpu().numpy(), oracle_conv(case)
+        assert np.array_equal(got, want), f"{SWEEP[i]} {mode}\n" + mismatch_report(got, want)
+
+
+def test_conv_strided_output_and_determinism():
+    case = gen.conv_case(77, 2, 32, 12, 12, 48, 3, 3, (1, 1), (1, 1, 1, 1))
+    _, x, y = gpu_conv(case, out_cstride=80)
+    got = y.cpu().numpy()[..., :48]
+    assert np.array_equal(got, oracle_conv(case))
+    op, x, y2 = gpu_conv(case, out_cstride=80)
+    y3 = op(x)
+    torch.cuda.synchronize()
+    assert np.array_equal(y2.cpu().numpy()[..., :48], y3.cpu().numpy()[..., :48])
+
+
+def test_conv_batch_shard_invariance():
+    """Images are independent: conv of a batch == concat of per-shard convs."""
+    case = gen.conv_case(78, 4, 64, 14, 14, 64, 3, 3, (1, 1), (1, 1, 1, 1))
+    _, _, y = gpu_conv(case)
+    full = y.cpu().numpy()
+    for lo, hi in [(0, 1), (1, 3), (3, 4)]:
+        sub = gen.ConvCase(**{**case.__dict__, "A": case.A[lo:hi]})
+        _, _, ys = gpu_conv(sub)
+        assert np.array_equal(ys.cpu().numpy(), full[lo:hi])
+
+
+@pytest.mark.parametrize("layer", resnet50_unique(), ids=lambda c: c.name)
+def test_resnet50_layers_batch1_full(layer):
+    case = gen.conv_case(1000 + zlib.crc32(layer.name.encode()) % 1000, 1, layer.C, layer.H, layer.W, layer.K, layer.R, layer.S,
+                         layer.stride, layer.pad, (1, 1), 1, "u8", "s8", relu=layer.relu)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), layer.name + "\n" + mismatch_report(got, want)
+
+
+@pytest.mark.parametrize("layer", [c for c in resnet50_unique() if c.name in
+                                   ("conv1", "layer1.0.conv2", "layer2.0.conv2", "layer3.1.conv1", "layer4.0.downsample",
+                                    "layer4.1.conv2")], ids=lambda c: c.name)
+@pytest.mark.parametrize("per_channel", [True, False])
+def test_resnet50_layers_batch64_sampled(layer, per_channel):
+    """Full-size (batch 64) launch; 4096 sampled outputs checked against the oracle
+    (per-tensor variant uses TFLite-style u8 weights with zp_W != 0)."""
+    wdt, zpW = ("s8", 0) if per_channel else ("u8", 128 + (zlib.crc32(layer.name.encode()) % 29) - 14)
+    case = gen.conv_case(2000 + zlib.crc32(layer.name.encode()) % 1000, 64, layer.C, layer.H, layer.W, layer.K, layer.R, layer.S,
+                         layer.stride, layer.pad, (1, 1), 1, "u8", wdt, zp_W=zpW, per_channel=per_channel,
+                         relu=layer.relu)
+    _, _, y = gpu_conv(case)
+    got = y.cpu().numpy().reshape(-1)
+    g = np.random.default_rng(3)
+    idx = g.choice(got.size, 4096, replace=False)
+    idx[:8] = [0, 1, got.size - 1, got.size - 2, layer.K - 1, layer.K, got.size // 2, got.size - layer.K]
+    want = oracle_conv_at(case, idx, layer.P, layer.Q)
+    assert np.array_equal(got[idx], want), layer.name
+
+
+def _dw_layers():
+    out, seen = [], set()
+    for c in mobilenet_v2_convs():
+        if c.groups > 1 and (c.C, c.stride) not in seen:
+            seen.add((c.C, c.stride))
+            out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("C,stride,act6,adt", [(16, 1, True, "u8"), (32, 2, False, "u8"), (144, 1, True, "u8"),
+                                               (12, 1, False, "s8"), (7, 2, True, "u8"), (96, 2, True, "s8")])
+def test_depthwise_small(C, stride, act6, adt):
+    for mode in ("upward", "tonearest"):
+        case = gen.conv_case(600 + C, 2, C, 13, 15, C, 3, 3, (stride, stride), (1, 1, 1, 1), (1, 1), C, adt, "s8",
+                             relu=True, act6=act6, rounding=mode)
+        _, _, y = gpu_conv(case)
+        got, want = y.cpu().numpy(), oracle_conv(case)
+        assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def test_depthwise_zpW_and_raw():
+    case = gen.conv_case(650, 1, 32, 9, 9, 32, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), 32, "u8", "u8", zp_W=120,
+                         per_channel=False, out_dtype="s32")
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case))
+
+
+@pytest.mark.parametrize("layer", _dw_layers(), ids=lambda c: f"{c.name}_C{c.C}_s{c.stride[0]}")
+def test_mobilenet_depthwise_batch128_sampled(layer):
+    case = gen.conv_case(3000 + layer.C, 128, layer.C, layer.H, layer.W, layer.K, 3, 3, layer.stride, layer.pad,
+                         (1, 1), layer.C, "u8", "s8", relu=True, act6=True)
+    _, _, y = gpu_conv(case)
+    got = y.cpu().numpy().reshape(-1)
+    idx = np.random.default_rng(4).choice(got.size, 4096, replace=False)
+    want = oracle_conv_at(case, idx, layer.P, layer.Q)
+    assert np.array_equal(got[idx], want)
+
+
+def test_errors_raise():
+    from paper_2006_10226_b200 import QnnError
+    case = gen.conv_case(700, 1, 8, 6, 6, 8, 3, 3, (1, 1), (1, 1, 1, 1), groups=2)
+    with pytest.raises(QnnError):
+        gpu_conv(case)
