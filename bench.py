@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — ResNet-50 int8 images/sec on the QNN hot path (BASELINE.json metric,
+configs[4]: full ResNet-50 pre-quantized int8 conv stack, synthetic weights).
+
+One step = one pass of the whole hot path over one batch (per GPU):
+  qnn_quantize (f32 image -> u8, Eq. 1)  ->  53 x qnn_conv2d (tcgen05 implicit
+  GEMM, folded zero-point terms, fused requantize + ReLU, Eq. 3 + Eq. 5)  ->
+  qnn_dense fc (raw int32)  ->  qnn_dequantize (logits -> f32).
+Glue ops that are not on the path (max pool, residual add, global avg pool)
+are not run; layers fed by them read persistent synthetic buffers.
+
+Contract: ``python bench.py --gpus N --steps K --warmup W`` (torchrun for N>1,
+one rank per GPU, batch sharded: every rank processes its own 256 images,
+weights replicated, no collective on the data path).  Rank 0 prints ONE JSON
+line.  ``--impl reference`` times the CPU oracle (the reference arm of this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "int8 conv TOPS (% of int8 TC peak) and ResNet-50 int8 images/sec at 1/2/4/8 B200"
+WORKLOAD = "configs[4]: ResNet-50 pre-quantized int8 conv stack (53 qnn.conv2d + qnn.dense fc), synthetic weights"
+
+
+# ----------------------------------------------------------------------------- model
+def resnet50_model(batch: int, seed: int = 4000):
+    """Synthetic pre-quantized ResNet-50: layer specs + numpy weights/biases/fresh inputs.
+
+    Recipe: u8 activations (zp from the producer, 0 after
+    ReLU, 128 otherwise), s8 symmetric per-channel weights U[-127,127] whose
+    scales s_W = U(0.5, 1.5) / unit keep the real activation scale ~constant,
+    int32 bias U[-4096,4096], output scale calibrated from input statistics,
+    UPWARD rounding, seed 4000 + layer index.
+    """
+    from paper_2006_10226_b200.stack import LayerSpec
+    from workloads import gen
+    from workloads.shapes import resnet50_convs, resnet50_fc
+
+    specs, weights, biases, fresh = [], {}, {}, {}
+    out_q = {}      # layer name -> (zp_out, s_out)
+    img_scale, img_zp = float(np.float32(4.77 / 255)), 128
+    for li, c in enumerate(resnet50_convs()):
+        g = gen.rng(seed + li)
+        if c.name == "conv1":
+            zp_A, s_A = img_zp, img_scale
+        elif c.src:
+            zp_A, s_A = out_q[c.src]
+        else:
+            zp_A, s_A = 0, 0.02
+            fresh[c.name] = gen.rand_q(g, (batch, c.H, c.W, c.C), "u8")
+        W = gen.rand_q(g, (c.K, c.R, c.S, c.C), "s8", -127, 127)
+        kk = c.C * c.R * c.S
+        # weight scales normalised so the real-valued activation scale stays ~constant
+        # through the chain (the role batch-norm folding plays in a trained network)
+        unit = gen.calibrated_out_scale(kk, (0, 255), zp_A, (-127, 127), 0, 1.0, 1.0)
+        s_W = (g.uniform(0.5, 1.5, size=c.K) / unit).astype(np.float32)
+        bias = g.integers(-4096, 4097, size=c.K).astype(np.int32)
+        s_out = gen.calibrated_out_scale(kk, (0, 255), zp_A, (-127, 127), 0, s_A, float(np.median(s_W)))
+        zp_out = 0 if c.relu else 128
+        out = dict(scale=s_out, zero_point=zp_out, dtype="u8", rounding="upward", relu=c.relu)
+        out_q[c.name] = (zp_out, s_out)
+        specs.append(LayerSpec(c.name, batch, c.H, c.W, c.C, c.K, c.R, c.S, c.stride, c.pad, 1, zp_A, s_A, 0,
+                               s_W, out, c.src))
+        weights[c.name] = W
+        biases[c.name] = bias
+    fin, fout = resnet50_fc()
+    g = gen.rng(seed + 99)
+    fc = dict(name="fc", zp_A=0, s_A=0.02, W=gen.rand_q(g, (fout, fin), "s8", -127, 127),
+              s_W=g.uniform(0.002, 0.02, size=fout).astype(np.float32),
+              bias=g.integers(-4096, 4097, size=fout).astype(np.int32),
+              A=gen.rand_q(g, (batch, fin), "u8"))
+    image = gen.rng(seed + 98).standard_normal((batch, 224, 224, 3)).astype(np.float32)
+    return dict(specs=specs, weights=weights, biases=biases, fresh=fresh, fc=fc, image=image,
+                img_scale=img_scale, img_zp=img_zp)
+
+
+class GpuResNet50:
+    def __init__(self, model, device):
+        import torch
+
+        from paper_2006_10226_b200 import qnn
+        from paper_2006_10226_b200.stack import ConvStack
+        self.torch = torch
+        self.qnn = qnn
+        dev = device
+        self.model = model
+        self.image_d = torch.from_numpy(model["image"]).to(dev)
+        self.q_image = torch.empty(self.image_d.shape, dtype=torch.uint8, device=dev)
+        fresh = {k: torch.from_numpy(v).to(dev) for k, v in model["fresh"].items()}
+        fresh["conv1"] = self.q_image
+        self.stack = ConvStack(model["specs"], {k: torch.from_numpy(v).to(dev) for k, v in model["weights"].items()},
+                               {k: torch.from_numpy(v).to(dev) for k, v in model["biases"].items()}, fresh, dev)
+        fc = model["fc"]
+        self.fc_in = torch.from_numpy(fc["A"]).to(dev)
+        self.fc = qnn.PackedDense(fc["A"].shape[0], torch.from_numpy(fc["W"]).to(dev),
+                                  torch.from_numpy(fc["bias"]).to(dev), fc["zp_A"], 0, fc["s_A"], fc["s_W"], None)
+        self.fc_out = torch.empty((fc["A"].shape[0], fc["W"].shape[0]), dtype=torch.int32, device=dev)
+        self.logit_scale = (np.float32(fc["s_A"]) * fc["s_W"].astype(np.float32)).astype(np.float32)
+        self.logits = torch.empty(self.fc_out.shape, dtype=torch.float32, device=dev)
+        self.graph = None
+
+    def step(self, events=None):
+        q = self.qnn
+        m = self.model
+        q.qnn_quantize(self.image_d, [m["img_scale"]], [m["img_zp"]], "u8", out=self.q_image)
+        self.stack.run(events=events)
+        self.fc(self.fc_in, out=self.fc_out)
+        q.qnn_dequantize(self.fc_out, self.logit_scale, [0], axis=-1, out=self.logits)
+
+    def capture(self):
+        torch = self.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.step()          # warm the attribute caches outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        self.qnn.launch_counter_reset()
+        with torch.cuda.graph(self.graph):
+            self.step()
+        self.launches_per_step = self.qnn.launch_counter()
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no_samples"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) arm
+def oracle_forward(model, n_img: int = 1):
+    """The oracle, as it stands, on n_img images of the same workload (NCHW)."""
+    import oracle as orc
+    outs = {}
+    img = model["image"][:n_img]
+    q_img = orc.quantize(img, [model["img_scale"]], [model["img_zp"]], "u8")
+    for sp in model["specs"]:
+        if sp.name == "conv1":
+            x = q_img
+        elif sp.src:
+            x = outs[sp.src]
+        else:
+            x = model["fresh"][sp.name][:n_img]
+        W = model["weights"][sp.name]
+        y = orc.qnn_conv2d(np.ascontiguousarray(x.transpose(0, 3, 1, 2)), np.ascontiguousarray(W.transpose(0, 3, 1, 2)),
+                           sp.zp_A, sp.zp_W, sp.s_A, sp.s_W, model["biases"][sp.name], sp.out, sp.stride, sp.pad)
+        outs[sp.name] = np.ascontiguousarray(y.transpose(0, 2, 3, 1))
+    fc = model["fc"]
+    acc = orc.qnn_dense(fc["A"][:n_img], fc["W"], fc["zp_A"], 0, fc["s_A"], fc["s_W"], fc["bias"], None)
+    scale = (np.float32(fc["s_A"]) * fc["s_W"]).astype(np.float32)
+    return orc.dequantize(acc, scale, [0], axis=-1), outs
+
+
+def cpu_baseline(model, n_img: int = 1):
+    import oracle as orc
+    t0 = time.perf_counter()
+    oracle_forward(model, n_img)
+    dt = time.perf_counter() - t0
+    return {"value": n_img / dt, "unit": "images/s", "cores": orc.num_threads(), "kind": "oracle",
+            "sample": f"{n_img} image(s) through the full stack (quantize, 53 conv, fc, dequantize), {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    model = resnet50_model(1)
+    if args.warmup > 0:
+        oracle_forward(model, 1)          # one untimed pass (bounded: the oracle is slow)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_forward(model, 1)
+        times.append(time.perf_counter() - t0)
+    import oracle as orc
+    tot = sum(times)
+    value = args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "per_step_sample": "1 image (bounded CPU sample of the 256-image step)",
+                       "global_batch": 1, "parallelism": "cpu oracle, rank 0 only"},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": orc.num_threads(), "kind": "oracle",
+                             "sample": f"{args.steps} steps x 1 image through the full stack"},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU per step")
+    ap.add_argument("--impl", default="qnn", choices=["qnn", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--breakdown-steps", type=int, default=5)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "contract: at least 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    model = resnet50_model(args.batch)
+    net = GpuResNet50(model, dev)
+    net.capture()
+    for _ in range(args.warmup):
+        net.replay()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K graph replays, inputs resident in HBM
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        net.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    images = args.batch * world * args.steps
+    value = images / (ms / 1000.0)
+
+    # ---------------- e2e: host f32 image in (pinned H2D) -> graph -> logits out (D2H), same metric
+    host_in = torch.from_numpy(model["image"]).pin_memory()
+    host_out = torch.empty(net.logits.shape, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    net.image_d.copy_(host_in, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        net.image_d.copy_(host_in, non_blocking=True)
+        net.replay()
+        host_out.copy_(net.logits, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ems = float(tt.item())
+    e2e_value = args.batch * world * e2e_steps / (ems / 1000.0)
+    h2d = host_in.numel() * 4
+    d2h = host_out.numel() * 4
+
+    # ---------------- per-layer breakdown (eager launches bracketed by CUDA events on the launching stream)
+    nl = len(net.stack.specs)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
+    fce = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    layer_ms = np.zeros(nl)
+    fc_ms = 0.0
+    for _ in range(args.breakdown_steps):
+        net.qnn.qnn_quantize(net.image_d, [model["img_scale"]], [model["img_zp"]], "u8", out=net.q_image)
+        net.stack.run(events=evs)
+        fce[0].record()
+        net.fc(net.fc_in, out=net.fc_out)
+        fce[1].record()
+        torch.cuda.synchronize()
+        layer_ms += np.array([a.elapsed_time(b) for a, b in evs])
+        fc_ms += fce[0].elapsed_time(fce[1])
+    layer_ms /= args.breakdown_steps
+    fc_ms /= args.breakdown_steps
+    macs = [sp.macs() for sp in net.stack.specs]
+    fc_macs = model["fc"]["A"].shape[0] * model["fc"]["W"].shape[0] * model["fc"]["W"].shape[1]
+    gemm_ms = float(layer_ms.sum() + fc_ms)
+    gemm_ops = 2.0 * (sum(macs) + fc_macs)
+    gemm_launches = nl + 1
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    bf16_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    int8_peak = 2.0 * bf16_sus       # nominal int8:bf16 = 4.5:2.25 (B200_PROFILING.md) x measured sustained bf16
+    achieved = gemm_ops / (gemm_ms / 1000.0) / 1e12
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        if tr.get("batch") == args.batch:
+            traffic = tr.get("bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    step_ops = 2.0 * (net.stack.total_macs() + fc_macs)
+    conv_tops = step_ops / (ms_per_step / 1000.0) / 1e12
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(model, 1)
+    layers = [{"name": sp.name, "ms": round(float(t), 4), "tops": round(2.0 * m / (t / 1000.0) / 1e12, 1)}
+              for sp, t, m in zip(net.stack.specs, layer_ms, macs)]
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": args.batch * world, "per_gpu_batch": args.batch,
+                   "image": "224x224x3 f32 -> u8", "parallelism": f"dp{world} (batch shard, replicated weights, "
+                   "no data-path collective)", "weights": "s8 symmetric per-channel", "activations": "u8",
+                   "rounding": "UPWARD", "l2": "no flush: per-step working set (154 MB f32 input + ~1.9 GB "
+                   "activations) exceeds the 126 MB L2", "graph": "CUDA graph replay per step"},
+        "conv_tops": round(conv_tops, 1), "conv_pct_int8_peak": round(100 * conv_tops / int8_peak, 2),
+        "e2e": {"value": round(e2e_value, 1), "unit": "images/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "note": "pinned f32 images H2D + graph + f32 logits D2H, serial per step"},
+        "gpu_launches": int(net.launches_per_step * args.steps),
+        "roofline": {"kernel": "qnn_gemm_i8_kernel (all 54 conv/fc launches of a step)", "bound": "tensor",
+                     "achieved": round(achieved, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
+                     "frac": round(achieved / int8_peak, 4),
+                     "peak_note": "int8 dense = 2 x measured sustained bf16 (MEASURED_PEAKS.json) per the guide's "
+                                  "nominal 4.5/2.25 ratio",
+                     "traffic": traffic, "launches_per_step": gemm_launches,
+                     "kernel_share_of_step": round(gemm_ms / ms_per_step, 3),
+                     "ops_per_step": gemm_ops},
+        "clocks": clk,
+        "cpu_baseline": cpu,
+        "layers": layers,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

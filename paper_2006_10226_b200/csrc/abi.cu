@@ -70,13 +70,14 @@ static void small_tensor_fixup(CUtensorMap* m, unsigned long long bytes) {
 }
 
 static bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
-                      uint32_t box_cols, uint32_t box_rows) {
+                      uint32_t box_cols, uint32_t box_rows, bool swizzle = true) {
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {pitch_bytes};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = p_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for((int)box_cols),
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              swizzle ? swizzle_for((int)box_cols) : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   small_tensor_fixup(m, pitch_bytes * rows);
   return r == CUDA_SUCCESS;
@@ -325,7 +326,6 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   pl.BN = round_up((d->K + pl.num_n - 1) / pl.num_n, 32);
   pl.Kpad = pl.num_n * pl.BN;
   pl.num_m = (int)((pl.M + kGemmBM - 1) / kGemmBM);
-  pl.stages = gemm_max_stages(pl.BK, pl.BN);
   pl.im2col = !(d->R == 1 && d->S == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_t == 0 && d->pad_l == 0 &&
                  d->pad_b == 0 && d->pad_r == 0);
   if (pl.im2col) {
@@ -340,6 +340,8 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   st = build_classes(pl.Q, d->W, d->S, d->stride_w, d->pad_l, d->dil_w, pl.ct.s_lo, pl.ct.s_hi, &pl.ct.ncc, pl.colcls);
   if (st != QNN_OK) return st;
   if (pl.ct.ncr * pl.ct.ncc > 255) return QNN_ERR_UNSUPPORTED;
+  pl.stages = gemm_max_stages(pl.BK, pl.BN, pl.ct.ncr * pl.ct.ncc);
+  if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, pl.ct.ncr * pl.ct.ncc) > 227 * 1024) return QNN_ERR_UNSUPPORTED;
 
   const int RS = d->R * d->S;
   size_t off = 0;
@@ -387,7 +389,8 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
 
   // per-channel multipliers m_k = s_A * s_W[k] / s_out (reading R3)
   const int nmult = pl.depthwise ? d->C : pl.Kpad;
-  std::vector<int32_t> mult(nmult, 0), rsh(nmult, 1);
+  // padding columns (k >= K) get M = 0 with a fast-path shift so they never force the generic epilogue
+  std::vector<int32_t> mult(nmult, 0), rsh(nmult, 33);
   if (pl.requant) {
     for (int k = 0; k < d->K; ++k) {
       const double m = ((double)d->input_scale * (double)d->kernel_scales[d->num_kernel_scales == 1 ? 0 : k]) /
@@ -495,6 +498,12 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)d->R * d->S * pl.Cw, (uint64_t)pl.Kpad,
                  (uint64_t)d->R * d->S * pl.Cw, pl.BK, pl.BN);
   if (!ok) return QNN_ERR_UNSUPPORTED;
+  // 8-bit output through per-warp TMA stores when the output pitch allows it
+  alignas(64) CUtensorMap tmC;
+  std::memset(&tmC, 0, sizeof(tmC));
+  const bool tma_store = pl.requant && (pl.out_cs % 16) == 0 && (reinterpret_cast<uintptr_t>(output) & 15) == 0;
+  if (tma_store && !encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 32, false))
+    return QNN_ERR_UNSUPPORTED;
 
   GemmParams p{};
   p.M = (int)pl.M;
@@ -520,20 +529,24 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   ep.rowcls = one_class ? nullptr : pk + pl.pk_rowcls;
   ep.colcls = one_class ? nullptr : pk + pl.pk_colcls;
   ep.ncc = pl.ct.ncc;
+  ep.ncls = pl.ct.ncr * pl.ct.ncc;
+  ep.tma_store = tma_store;
   ep.rowsum = rowsum;
   ep.zpW = d->kernel_zero_point;
   ep.out = output;
   ep.out_pitch = pl.out_cs;
   ep.Kpad = pl.Kpad;
   ep.out_dtype = pl.requant ? (int)pl.out_dt : DT_S32;
-  ep.requant = pl.requant;
-  ep.mode = pl.mode;
   ep.zp_out = pl.zp_out;
   ep.lo = pl.lo;
   ep.hi = pl.hi;
   const int tiles = pl.num_m * pl.num_n;
   const int grid = std::min(tiles, sm_count());
-  return cuda_status(launch_gemm(tmA, tmB, p, grid, s));
+  int64_t qlo = INT32_MIN, qhi = INT32_MAX;
+  if (pl.requant) dtype_range(pl.out_dt, &qlo, &qhi);
+  const bool clamp = pl.requant && (pl.lo > qlo || pl.hi < qhi);
+  const int mode = pl.requant ? pl.mode : 2;
+  return cuda_status(launch_gemm(tmA, tmB, tmC, p, mode, clamp, grid, s));
 }
 
 // dense -> 1x1 conv over an M x 1 x 1 "image batch"

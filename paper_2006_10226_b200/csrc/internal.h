@@ -27,12 +27,11 @@ struct GemmEpilogue {
   const int32_t* rowsum;   // [M] Term-3 row sums (nullptr when zp_W == 0)
   void* out;
   long long out_pitch;     // elements between consecutive output pixels
-  int ncc;                 // number of column classes
+  int ncls, ncc;           // number of border classes, of column classes
   int Kpad;
   int32_t zpW;
   int out_dtype;           // DT_U8 / DT_S8 / DT_S32
-  int requant;             // 0 => raw int32 (Eq. 3 + bias)
-  int mode;                // rounding
+  int tma_store;           // 8-bit output through per-warp TMA stores (pitch % 16 == 0)
   int32_t zp_out, lo, hi;  // lo/hi already include ReLU, act clamp and dtype range
 };
 
@@ -51,10 +50,11 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmEpiWarps = 8;
 constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
 
-size_t gemm_smem_bytes(int BK, int BN, int stages);
-int gemm_max_stages(int BK, int BN);
-cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p, int grid,
-                        cudaStream_t stream);
+// epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls);
+int gemm_max_stages(int BK, int BN, int ncls);
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                        const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // Prepack / auxiliary kernels (prep.cu)

@@ -80,6 +80,30 @@ def test_conv_sweep(i):
         assert np.array_equal(got, want), f"{SWEEP[i]} {mode}\n" + mismatch_report(got, want)
 
 
+@pytest.mark.parametrize("mode", ["upward", "tonearest"])
+def test_conv_generic_requant_path(mode):
+    """Channels whose multiplier is outside the epilogue's mulhi fast range
+    (m >= 2^-1, i.e. right shift <= 32, or m < 2^-21) force the generic 64-bit
+    rounding for the whole tile; small operands keep outputs unsaturated."""
+    g = np.random.default_rng(91)
+    N, H, W, C, K = 2, 9, 9, 32, 64
+    A = (128 + g.integers(-3, 4, size=(N, H, W, C))).astype(np.uint8)
+    Wt = g.integers(-1, 2, size=(K, 3, 3, C)).astype(np.int8)
+    s_A, s_out = 0.05, 0.04
+    s_W = np.full(K, 0.003, np.float32)
+    s_W[0] = 0.9            # m = 1.125 -> shift 1  (rsh 30)
+    s_W[1] = 0.5            # m = 0.625 -> rsh 31
+    s_W[2] = 0.33           # m ~ 0.41  -> rsh 32
+    s_W[3] = 1e-7           # m ~ 1.2e-7 -> rsh 54 (> 52)
+    bias = g.integers(-20, 21, size=K).astype(np.int32)
+    case = gen.ConvCase(A, Wt, bias, 128, 0, s_A, s_W, s_out, 128, "u8", (1, 1), (1, 1, 1, 1), (1, 1), 1, False,
+                        None, None, mode)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
+    assert len(np.unique(want[..., 0])) > 5          # channel 0 is not saturated
+
+
 def test_conv_strided_output_and_determinism():
     case = gen.conv_case(77, 2, 32, 12, 12, 48, 3, 3, (1, 1), (1, 1, 1, 1))
     _, x, y = gpu_conv(case, out_cstride=80)
