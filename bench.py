@@ -326,21 +326,30 @@ def main():
     h2d = host_in.numel() * 4
     d2h = host_out.numel() * 4
 
-    # ---------------- per-layer breakdown (eager launches bracketed by CUDA events on the launching stream)
+    # ---------------- per-layer breakdown: each layer captured as its own CUDA graph and
+    # replayed back to back, bracketed by CUDA events on the launching stream (no host gaps)
     nl = len(net.stack.specs)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
-    fce = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    layer_graphs = []
+    for sp in net.stack.specs:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            net.stack.ops[sp.name](net.stack.inputs[sp.name], out=net.stack.outs[sp.name])
+        layer_graphs.append(g)
+    fc_graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(fc_graph):
+        net.fc(net.fc_in, out=net.fc_out)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl + 1)]
     layer_ms = np.zeros(nl)
     fc_ms = 0.0
     for _ in range(args.breakdown_steps):
-        net.qnn.qnn_quantize(net.image_d, [model["img_scale"]], [model["img_zp"]], "u8", out=net.q_image)
-        net.stack.run(events=evs)
-        fce[0].record()
-        net.fc(net.fc_in, out=net.fc_out)
-        fce[1].record()
+        for i, g in enumerate(layer_graphs + [fc_graph]):
+            evs[i][0].record()
+            g.replay()
+            evs[i][1].record()
         torch.cuda.synchronize()
-        layer_ms += np.array([a.elapsed_time(b) for a, b in evs])
-        fc_ms += fce[0].elapsed_time(fce[1])
+        t = np.array([a.elapsed_time(b) for a, b in evs])
+        layer_ms += t[:nl]
+        fc_ms += t[nl]
     layer_ms /= args.breakdown_steps
     fc_ms /= args.breakdown_steps
     macs = [sp.macs() for sp in net.stack.specs]

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -173,8 +174,11 @@ struct ConvPlan {
   int in_cs = 0, out_cs = 0;
   // tensor-core path
   bool pad_copy = false;
+  bool fold = false;     // width fold: (s, c) -> channels of a copy, filter becomes R x 1 (small-C stems)
   int Ct = 0;            // channel count / pitch seen by TMA
-  int BK = 0, nchunks = 0, Cw = 0, BN = 0, Kpad = 0, num_n = 0, num_m = 0, stages = 0;
+  // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
+  int gW = 0, gS = 0, g_sw = 0, g_pl = 0, g_pr = 0, g_dw = 0;
+  int BK = 0, nchunks = 0, Cw = 0, BN = 0, Kpad = 0, num_n = 0, num_m = 0, stages = 0, b_res_kb = 0, kps = 1;
   bool im2col = false;
   ClassTable ct{};
   std::vector<uint8_t> rowcls, colcls;
@@ -307,8 +311,16 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
 
   // ------------------------------------------------------------ tensor-core plan
   const bool tma_pitch_ok = (pl.in_cs % 16) == 0;
-  pl.pad_copy = !tma_pitch_ok;
-  pl.Ct = pl.pad_copy ? round_up(d->C, 16) : d->C;
+  pl.gW = d->W; pl.gS = d->S; pl.g_sw = d->stride_w; pl.g_pl = d->pad_l; pl.g_pr = d->pad_r; pl.g_dw = d->dil_w;
+  pl.fold = (!tma_pitch_ok || d->C < 16) && d->S > 1 && d->S * d->C <= 128 && (long long)d->W * d->C <= 48 * 1024;
+  if (pl.fold) {
+    // X'[n, h, q, s*C + c] = A[n, h, q*sw + s*dw - pl, c] (0 outside): an R x 1 conv over X'
+    pl.Ct = round_up(d->S * d->C, 16);
+    pl.gW = (int)Qn; pl.gS = 1; pl.g_sw = 1; pl.g_pl = 0; pl.g_pr = 0; pl.g_dw = 1;
+  } else {
+    pl.pad_copy = !tma_pitch_ok;
+    pl.Ct = pl.pad_copy ? round_up(d->C, 16) : d->C;
+  }
   {
     int best_bk = 128, best = INT32_MAX;
     for (int bk : {128, 64, 32}) {
@@ -326,27 +338,38 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   pl.BN = round_up((d->K + pl.num_n - 1) / pl.num_n, 32);
   pl.Kpad = pl.num_n * pl.BN;
   pl.num_m = (int)((pl.M + kGemmBM - 1) / kGemmBM);
-  pl.im2col = !(d->R == 1 && d->S == 1 && d->stride_h == 1 && d->stride_w == 1 && d->pad_t == 0 && d->pad_l == 0 &&
-                 d->pad_b == 0 && d->pad_r == 0);
+  pl.im2col = !(d->R == 1 && pl.gS == 1 && d->stride_h == 1 && pl.g_sw == 1 && d->pad_t == 0 && pl.g_pl == 0 &&
+                 d->pad_b == 0 && pl.g_pr == 0);
   if (pl.im2col) {
-    const int lw = -d->pad_l, lh = -d->pad_t;
-    const int uw = d->pad_r - (d->S - 1) * d->dil_w, uh = d->pad_b - (d->R - 1) * d->dil_h;
+    const int lw = -pl.g_pl, lh = -d->pad_t;
+    const int uw = pl.g_pr - (pl.gS - 1) * pl.g_dw, uh = d->pad_b - (d->R - 1) * d->dil_h;
     if (lw < -128 || lh < -128 || uw < -128 || uh < -128 || uw > 127 || uh > 127) return QNN_ERR_UNSUPPORTED;
-    if ((d->R - 1) * d->dil_h > 255 || (d->S - 1) * d->dil_w > 255) return QNN_ERR_UNSUPPORTED;
-    if (d->stride_h > 8 || d->stride_w > 8) return QNN_ERR_UNSUPPORTED;
+    if ((d->R - 1) * d->dil_h > 255 || (pl.gS - 1) * pl.g_dw > 255) return QNN_ERR_UNSUPPORTED;
+    if (d->stride_h > 8 || pl.g_sw > 8) return QNN_ERR_UNSUPPORTED;
   }
   st = build_classes(pl.P, d->H, d->R, d->stride_h, d->pad_t, d->dil_h, pl.ct.r_lo, pl.ct.r_hi, &pl.ct.ncr, pl.rowcls);
   if (st != QNN_OK) return st;
   st = build_classes(pl.Q, d->W, d->S, d->stride_w, d->pad_l, d->dil_w, pl.ct.s_lo, pl.ct.s_hi, &pl.ct.ncc, pl.colcls);
   if (st != QNN_OK) return st;
   if (pl.ct.ncr * pl.ct.ncc > 255) return QNN_ERR_UNSUPPORTED;
-  pl.stages = gemm_max_stages(pl.BK, pl.BN, pl.ct.ncr * pl.ct.ncc);
-  if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, pl.ct.ncr * pl.ct.ncc) > 227 * 1024) return QNN_ERR_UNSUPPORTED;
+  {
+    const int ncls = pl.ct.ncr * pl.ct.ncc;
+    const int num_kb = d->R * pl.gS * pl.nchunks;
+    // keep the whole weight operand resident when it is one N tile and leaves room for >= 4 A stages
+    pl.b_res_kb = 0;
+    if (pl.num_n == 1 && gemm_smem_bytes(pl.BK, pl.BN, 4, ncls, num_kb, 1) <= 227 * 1024) pl.b_res_kb = num_kb;
+    // k-blocks per stage: about 32 KB of operands per barrier round trip, at least 3 stages
+    const int per_kb = kGemmBM * pl.BK + (pl.b_res_kb ? 0 : pl.BN * pl.BK);
+    pl.kps = std::max(1, std::min(num_kb, 32768 / per_kb));
+    while (pl.kps > 1 && gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, pl.kps) < 3) --pl.kps;
+    pl.stages = gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, pl.kps);
+    if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, ncls, pl.b_res_kb, pl.kps) > 227 * 1024) return QNN_ERR_UNSUPPORTED;
+  }
 
-  const int RS = d->R * d->S;
+  const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
-  off = align256(off + (size_t)pl.Kpad * RS * pl.Cw);
+  off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
   pl.pk_off = off;
   off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
   pl.pk_mult = off;
@@ -360,9 +383,9 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   pl.pk_total = off;
 
   size_t w = 0;
-  if (pl.pad_copy) {
+  if (pl.pad_copy || pl.fold) {
     pl.ws_pad = w;
-    w = align256(w + (size_t)d->N * d->H * d->W * pl.Ct);
+    w = align256(w + (size_t)d->N * d->H * pl.gW * pl.Ct);
   }
   if (d->kernel_zero_point != 0) {
     pl.ws_pixsum = w;
@@ -409,7 +432,11 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
       e = cudaMemsetAsync(pk + pl.pk_bias, 0, (size_t)d->C * 4, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
   } else {
-    e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
+    // folded: each filter row r is one GEMM tap whose S*C channels are contiguous in OHWI
+    if (pl.fold)
+      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R, d->S * d->C, pl.Cw, pl.Kpad, s);
+    else
+      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
                             pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off), pl.Kpad, s);
@@ -464,7 +491,13 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   cudaError_t e;
   const void* A = input;
   long long a_pitch = pl.in_cs;
-  if (pl.pad_copy) {
+  if (pl.fold) {
+    e = launch_fold_width(input, pl.in_cs, wsb + pl.ws_pad, d->N, d->H, d->W, d->C, pl.Q, d->S, d->stride_w, d->pad_l,
+                          d->dil_w, pl.Ct, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    A = wsb + pl.ws_pad;
+    a_pitch = pl.Ct;
+  } else if (pl.pad_copy) {
     e = launch_pad_channels(input, pl.in_cs, wsb + pl.ws_pad, pl.Ct, (long long)d->N * d->H * d->W, d->C, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     A = wsb + pl.ws_pad;
@@ -488,38 +521,66 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
 
   alignas(64) CUtensorMap tmA, tmB;
   bool ok;
+  const int a_chan = (pl.pad_copy || pl.fold) ? pl.Ct : d->C;
+  const int taps = d->R * pl.gS;
   if (pl.im2col)
-    ok = encode_im2col(&tmA, A, pl.pad_copy ? pl.Ct : d->C, d->W, d->H, d->N, (uint64_t)a_pitch, -d->pad_l, -d->pad_t,
-                       d->pad_r - (d->S - 1) * d->dil_w, d->pad_b - (d->R - 1) * d->dil_h, pl.BK, d->stride_w,
+    ok = encode_im2col(&tmA, A, a_chan, pl.gW, d->H, d->N, (uint64_t)a_pitch, -pl.g_pl, -d->pad_t,
+                       pl.g_pr - (pl.gS - 1) * pl.g_dw, d->pad_b - (d->R - 1) * d->dil_h, pl.BK, pl.g_sw,
                        d->stride_h);
   else
-    ok = encode_2d(&tmA, A, (uint64_t)(pl.pad_copy ? pl.Ct : d->C), (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmBM);
+    ok = encode_2d(&tmA, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmBM);
   if (!ok) return QNN_ERR_UNSUPPORTED;
-  ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)d->R * d->S * pl.Cw, (uint64_t)pl.Kpad,
-                 (uint64_t)d->R * d->S * pl.Cw, pl.BK, pl.BN);
+  ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)taps * pl.Cw, (uint64_t)pl.Kpad, (uint64_t)taps * pl.Cw, pl.BK,
+                 pl.BN);
   if (!ok) return QNN_ERR_UNSUPPORTED;
   // 8-bit output through per-warp TMA stores when the output pitch allows it
-  alignas(64) CUtensorMap tmC;
-  std::memset(&tmC, 0, sizeof(tmC));
-  const bool tma_store = pl.requant && (pl.out_cs % 16) == 0 && (reinterpret_cast<uintptr_t>(output) & 15) == 0;
-  if (tma_store && !encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 32, false))
-    return QNN_ERR_UNSUPPORTED;
+  // one store box per epilogue column half: 32 rows x (that half's columns), swizzled to match
+  // the staging layout (32/64/128-B rows), dense for 96-B rows
+  alignas(64) CUtensorMap tmC[4];
+  std::memset(tmC, 0, sizeof(tmC));
+  static const bool no_tma_store = std::getenv("QNN_NO_TMA_STORE") != nullptr;   // profiling switch
+  const bool tma_store = !no_tma_store && pl.requant && (pl.out_cs % 16) == 0 &&
+                         (reinterpret_cast<uintptr_t>(output) & 15) == 0;
+  if (tma_store) {
+    const int nchunk = pl.BN / 32, ng = kGemmEpiWarps / 4;
+    for (int h = 0; h < ng; ++h) {
+      const int width = ((h + 1) * nchunk / ng - h * nchunk / ng) * 32;
+      const int wb = width ? width : 32;
+      const bool swz = wb == 32 || wb == 64 || wb == 128;
+      if (!encode_2d(&tmC[h], output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, wb, 32, swz))
+        return QNN_ERR_UNSUPPORTED;
+    }
+  }
 
   GemmParams p{};
   p.M = (int)pl.M;
   p.Nout = d->K;
   p.nchunks = pl.nchunks;
-  p.num_kb = d->R * d->S * pl.nchunks;
-  p.S = d->S;
+  p.num_kb = taps * pl.nchunks;
+  p.S = pl.gS;
   p.dil_h = d->dil_h;
-  p.dil_w = d->dil_w;
+  p.dil_w = pl.g_dw;
   p.BK = pl.BK;
   p.BN = pl.BN;
   p.stages = pl.stages;
   p.num_m_tiles = pl.num_m;
   p.num_n_tiles = pl.num_n;
   p.im2col = pl.im2col;
-  p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = d->stride_w; p.pt = d->pad_t; p.pl = d->pad_l;
+  p.b_res = pl.b_res_kb > 0;
+  p.kps = pl.kps;
+  p.a_base = reinterpret_cast<const uint8_t*>(A);
+  p.a_pitch = a_pitch;
+  p.H = d->H;
+  p.W = pl.gW;
+  p.a_halo = (d->R - 1) * d->dil_h;
+  {
+    static const char* dbg_env = std::getenv("QNN_GEMM_DEBUG");
+    p.dbg = dbg_env ? std::atoi(dbg_env) : 0;
+    // QNN_GEMM_TRACE=<device address of a zeroed 64 KiB buffer>: CTA 0 records clock64 events
+    static const char* tr_env = std::getenv("QNN_GEMM_TRACE");
+    p.trace = tr_env ? reinterpret_cast<unsigned long long*>(std::strtoull(tr_env, nullptr, 0)) : nullptr;
+  }
+  p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = pl.g_sw; p.pt = d->pad_t; p.pl = pl.g_pl;
   p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8, kGemmBM, pl.BN);
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);

@@ -29,21 +29,27 @@
 
 namespace qnn {
 
-constexpr int kStageOutBytes = kGemmEpiWarps * 2 * 1024;  // per-warp double-buffered 32x32 B staging
-constexpr int kParamBytes = 256 * 16;                     // per-column {0, c, M, t}
+constexpr int kEpiGroups = kGemmEpiWarps / 4;             // column groups (4 warps each cover the 128 rows)
+constexpr int kStageOutBytes = kGemmEpiWarps * 4 * 1024;  // per-warp 2 x (32 rows x <= 64 B) output staging
+constexpr int kParamBytes = 256 * 8 + 256 * 8;            // per-column {M, t} and (c << 32)
 
 // per-class offset rows in smem: pitch BN + 4 ints keeps rows 16-B aligned and spreads banks
 static __host__ __device__ inline size_t off_table_bytes(int ncls, int BN) { return (size_t)ncls * (BN + 4) * 4; }
 
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls) {
-  return 1024 + (size_t)stages * ((size_t)kGemmBM * BK + (size_t)BN * BK) + kStageOutBytes + kParamBytes +
-         off_table_bytes(ncls, BN) + 256;
+// b_res_kb > 0: the whole B operand (b_res_kb k-blocks) stays resident in smem and
+// the pipeline stages carry A only.
+// Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
+// commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps) {
+  const size_t a = (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
+  const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * b : stages * (a + b * kps);
+  return 1024 + ring + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 256;
 }
 
-int gemm_max_stages(int BK, int BN, int ncls) {
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps) {
   const size_t budget = 227 * 1024;
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls) > budget) --s;
+  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps) > budget) --s;
   return s;
 }
 
@@ -76,6 +82,30 @@ __device__ __forceinline__ void tmem_load32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
         "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+// Split TMEM load / wait for software pipelining: the wait takes the destination
+// registers as in/out operands so no use of them can be scheduled before it.
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
 }
 __device__ __forceinline__ uint32_t pack4_u8(int a, int b, int c, int d) {
   uint32_t o;
@@ -111,75 +141,122 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Requantize 32 accumulators of one row (this lane) against 32 consecutive columns.
-// prm[i] = {0, c, M, t}: the (0, c) pair is the 64-bit addend of IMAD.HI, so
-// mulhi(v, M) + c is a single instruction.  offc: 32 per-column int32 offsets
-// (16-B aligned, read 4 at a time).
-template <int MODE, bool CLAMP, bool FAST>
-__device__ __forceinline__ void requant_row32(const uint32_t (&acc)[32], const int4* __restrict__ prm,
-                                              const int4* __restrict__ offc, int32_t rterm, int32_t zp_out,
-                                              int32_t lo, int32_t hi, int32_t (&y)[32]) {
+// Fixed-point requantize of one accumulator column value (reading R1/R2/R15).
+//   Fast UPWARD:    r = (mulhi(v, M) + c) >> t            c = 2^(t-1) + zp_out*2^t
+//   Fast TONEAREST: r = sign(v) * ((mulhi(|v|, M) + c) >> t) + zp_out,  c = 2^(t-1)
+//   Generic:        64-bit rounding shift by rsh (t holds -rsh, or t = rsh - 32)
+template <int MODE, bool FAST>
+__device__ __forceinline__ int32_t rq1(int32_t v, int32_t M, int32_t t, int32_t c, int32_t zp_out) {
+  if (FAST) {
+    if (MODE == 0) {
+      return (__mulhi(v, M) + c) >> t;
+    } else {
+      const uint32_t a = v < 0 ? 0u - (uint32_t)v : (uint32_t)v;
+      const int32_t m = (int32_t)((__umulhi(a, (uint32_t)M) + (uint32_t)c) >> t);
+      return (v < 0 ? -m : m) + zp_out;
+    }
+  } else {
+    const int rsh = t > 0 ? t + 32 : -t;
+    return (int32_t)(rq_round((int64_t)v * M, rsh, MODE) + zp_out);
+  }
+}
+
+// One 32-column chunk of one row: offsets, requantize, clamp; packed to 8-bit words
+// (MODE 0/1) or kept as int32 (MODE 2, raw).  Parameters are read four columns per
+// broadcast LDS.128: mt = {M, t} pairs, cc = c, off = folded offsets.
+template <int MODE, bool CLAMP, bool FAST, bool S8OUT>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const int4* __restrict__ off4,
+                                          const int4* __restrict__ mt4, const int4* __restrict__ c4,
+                                          int32_t rterm, int32_t zp_out, int32_t lo, int32_t hi,
+                                          uint32_t (&w)[8], int32_t* y) {
 #pragma unroll
-  for (int i4 = 0; i4 < 8; ++i4) {
-    const int4 o4 = offc[i4];
-    const int32_t offs[4] = {o4.x, o4.y, o4.z, o4.w};
+  for (int q4 = 0; q4 < 8; ++q4) {
+    const int4 o = off4[q4];
+    const int32_t offs[4] = {o.x, o.y, o.z, o.w};
+    int32_t yy[4];
+    if (MODE == 2) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i4 * 4 + j;
-      const int32_t v = (int32_t)(acc[i] + (uint32_t)offs[j] - (uint32_t)rterm);  // wrap-exact (reading R10)
-      int32_t r;
-      if (MODE == 2) {
-        r = v;
-      } else {
-        const int4 q = prm[i];  // same address across the warp -> broadcast
-        if (FAST) {
-          if (MODE == 0) {
-            r = (__mulhi(v, q.z) + q.y) >> q.w;
-          } else {
-            const uint32_t a = v < 0 ? (uint32_t)(-(int64_t)v) : (uint32_t)v;
-            const int32_t m = (int32_t)((__umulhi(a, (uint32_t)q.z) + (uint32_t)q.y) >> q.w);
-            r = (v < 0 ? -m : m) + zp_out;
-          }
-        } else {
-          // generic 64-bit path (tile has a column outside the fast range); q.w holds
-          // t = rsh - 32 for fast-range columns and -rsh for the others
-          const int rsh = q.w > 0 ? q.w + 32 : -q.w;
-          r = (int32_t)(rq_round((int64_t)v * q.z, rsh, MODE) + zp_out);
-        }
+      for (int u = 0; u < 4; ++u) yy[u] = (int32_t)(v[q4 * 4 + u] + (uint32_t)offs[u] - (uint32_t)rterm);
+    } else {
+      const int4 mtA = mt4[q4 * 2], mtB = mt4[q4 * 2 + 1], cq = c4[q4];
+      const int32_t Ms[4] = {mtA.x, mtA.z, mtB.x, mtB.z}, Ts[4] = {mtA.y, mtA.w, mtB.y, mtB.w};
+      const int32_t Cs[4] = {cq.x, cq.y, cq.z, cq.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t vv = (int32_t)(v[q4 * 4 + u] + (uint32_t)offs[u] - (uint32_t)rterm);  // wrap-exact (R10)
+        int32_t r = rq1<MODE, FAST>(vv, Ms[u], Ts[u], Cs[u], zp_out);
         if (CLAMP) r = min(max(r, lo), hi);
+        yy[u] = r;
       }
-      y[i] = r;
+    }
+    if (MODE == 2) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[q4 * 4 + u] = yy[u];
+    } else {
+      w[q4] = S8OUT ? pack4_s8(yy[0], yy[1], yy[2], yy[3]) : pack4_u8(yy[0], yy[1], yy[2], yy[3]);
     }
   }
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP>
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
+  if (tr && blockIdx.x == 0) tr[slot] = clock64();
+}
+
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     qnn_gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmParams p) {
+                       const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
+                       const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmC3,
+                       const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base (SW128 atoms); pointer arithmetic on the __shared__ array keeps the address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int BK = p.BK, BN = p.BN, stages = p.stages;
   const uint32_t a_bytes = kGemmBM * BK, b_bytes = BN * BK;
+  const bool b_res = p.b_res;
+  const int kps = p.kps;                   // k-blocks per pipeline stage
   uint8_t* sA = smem;
-  uint8_t* sB = smem + stages * a_bytes;
-  uint8_t* sOut = sB + stages * b_bytes;
-  int4* sPrm = reinterpret_cast<int4*>(sOut + kStageOutBytes);
-  int32_t* sOff = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(sPrm) + kParamBytes);
+  uint8_t* sB = smem + (size_t)stages * kps * a_bytes;   // ring of B stages, or the resident B (num_kb blocks)
+  uint8_t* sOut = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);
+  const bool tracing = p.trace != nullptr && blockIdx.x == 0;
+  int2* sMT = reinterpret_cast<int2*>(sOut + kStageOutBytes);          // {M, t} per column
+  int32_t* sCC = reinterpret_cast<int32_t*>(sMT + 256);               // c per column
+  int32_t* sOff = sCC + 512;
   const int ncls = HAS_CLS ? p.e.ncls : 1;
   const int offp = BN + 4;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sOff) + off_table_bytes(ncls, BN));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres_full = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
+  // Warp roles.  The warp scheduler favours higher warp ids, so the latency-critical
+  // single-thread roles get the highest ids and are never starved by waiting epilogue warps.
+  constexpr int kEpiW = kGemmEpiWarps;        // epilogue warps 0..15
+  constexpr int kAllocWarp = kEpiW + 1;       // TMEM allocator
+  constexpr int kProdWarp = kEpiW + 2;        // TMA producer
+  constexpr int kMmaWarp = kEpiW + 3;         // MMA issuer
+  if (warp == kProdWarp && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (p.e.tma_store) tma_prefetch_desc(&tmC);
+    if (p.e.tma_store) {
+      tma_prefetch_desc(&tmC0);
+      tma_prefetch_desc(&tmC1);
+      tma_prefetch_desc(&tmC2);
+      tma_prefetch_desc(&tmC3);
+    }
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -188,102 +265,154 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kGemmEpiWarps);
     }
+    mbar_init(bres_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x == 0) trace_at(p.trace, 6000);
+  if (warp == kAllocWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_at(p.trace, 6001);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_blk = t / p.num_n_tiles, n_blk = t - m_blk * p.num_n_tiles;
-        const int m0 = m_blk * kGemmBM;
-        int an = 0, ah = 0, aw = 0;
-        if (p.im2col) {
-          const int pq = p.P * p.Q;
-          const int n0 = m0 / pq, rem = m0 - n0 * pq;
-          const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
-          an = n0;
-          ah = p0 * p.sh - p.pt;
-          aw = q0 * p.sw - p.pl;
+    // The whole warp runs the loop (warp-uniform control flow keeps coordinates and
+    // descriptor addresses in uniform registers); one elected lane issues.
+    const bool leader = elect_one();
+    if (b_res && blockIdx.x < num_tiles) {
+      // weights are shared by every tile of this CTA: load them once
+      if (leader) {
+        mbar_arrive_expect_tx(bres_full, (uint32_t)p.num_kb * b_bytes);
+        for (int kb = 0; kb < p.num_kb; ++kb) tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, 0);
+      }
+      __syncwarp();
+    }
+    int stage = 0, it_p = 0;
+    uint32_t phase = 0;
+    const bool skip_a = p.dbg & 4;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m_blk = t / p.num_n_tiles, n_blk = t - m_blk * p.num_n_tiles;
+      const int m0 = m_blk * kGemmBM;
+      int an = 0, ah = 0, aw = 0;
+      if (p.im2col) {
+        const int pq = p.P * p.Q;
+        const int n0 = m0 / pq, rem = m0 - n0 * pq;
+        const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
+        an = n0;
+        ah = p0 * p.sh - p.pt;
+        aw = q0 * p.sw - p.pl;
+      }
+      // (filter row, filter col, channel chunk) of the next k-block, advanced by counters
+      int kr = 0, ks = 0, kc = 0;
+      for (int kb0 = 0; kb0 < p.num_kb; kb0 += kps) {
+        const int nk = min(kps, p.num_kb - kb0);
+        if (tracing && leader && it_p < 256) trace_at(p.trace, 6300 + it_p);
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) {
+          if (tracing && it_p < 2048) trace_at(p.trace, it_p);
+          mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * ((b_res ? 0 : b_bytes) + (skip_a ? 0 : a_bytes)));
+          uint8_t* dA = sA + (size_t)(stage * kps) * a_bytes;
+          uint8_t* dB = sB + (size_t)(stage * kps) * b_bytes;
+          for (int t2 = 0; t2 < nk; ++t2, dA += a_bytes, dB += b_bytes) {
+            const int kb = kb0 + t2;
+            if (skip_a) {
+            } else if (p.im2col) {
+              tma_load_im2col_4d(dA, &tmA, &full[stage], kc * BK, aw, ah, an, (uint16_t)(ks * p.dil_w),
+                                 (uint16_t)(kr * p.dil_h));
+            } else {
+              tma_load_2d(dA, &tmA, &full[stage], kb * BK, m0);
+            }
+            if (!b_res) tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
+            if (++kc == p.nchunks) {
+              kc = 0;
+              if (++ks == p.S) {
+                ks = 0;
+                ++kr;
+              }
+            }
+          }
+          if (tracing && it_p < 256) trace_at(p.trace, 6600 + it_p);
         }
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
-          uint8_t* dA = sA + stage * a_bytes;
-          uint8_t* dB = sB + stage * b_bytes;
-          if (p.im2col) {
-            const int tap = kb / p.nchunks, ch = kb - tap * p.nchunks;
-            const int r = tap / p.S, s = tap - r * p.S;
-            tma_load_im2col_4d(dA, &tmA, &full[stage], ch * BK, aw, ah, an, (uint16_t)(s * p.dil_w),
-                               (uint16_t)(r * p.dil_h));
-          } else {
-            tma_load_2d(dA, &tmA, &full[stage], kb * BK, m0);
-          }
-          tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
-          if (++stage == stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        __syncwarp();
+        ++it_p;
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
-    __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // Warp-uniform loop; the elected lane issues every tcgen05.mma and its commits.
+    const bool leader = elect_one();
+    int stage = 0, it_m = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    const uint64_t adesc0 = make_sdesc(smem_u32(sA), BK);
+    const uint64_t bdesc0 = make_sdesc(smem_u32(sB), BK);
+    const int ksteps = (p.dbg & 8) ? 0 : BK / 32;
+    if (b_res) mbar_wait(bres_full, 0);
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      if (tracing && leader && it < 100) trace_at(p.trace, 7200 + it);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      if (tracing && leader && it < 100) trace_at(p.trace, 7300 + it);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * 256;
+      for (int kb0 = 0; kb0 < p.num_kb; kb0 += kps) {
+        const int nk = min(kps, p.num_kb - kb0);
+        if (tracing && leader && it_m < 256) trace_at(p.trace, 6900 + it_m);
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * a_bytes);
-          const uint32_t b_addr = smem_u32(sB + stage * b_bytes);
-          for (int k = 0; k < BK / 32; ++k) {
-            umma_i8(d_tmem, make_sdesc(a_addr + k * 32, BK), make_sdesc(b_addr + k * 32, BK), p.idesc,
-                    (kb | k) != 0);
+        if (leader) {
+          if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
+          for (int t = 0; t < nk; ++t) {
+            const int kb = kb0 + t;
+            // descriptors advance by (byte offset >> 4) in the start-address field
+            const uint64_t ad = adesc0 + (((uint32_t)(stage * kps + t) * a_bytes) >> 4);
+            const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb : stage * kps + t) * b_bytes) >> 4);
+            for (int k = 0; k < ksteps; ++k) umma_i8(d_tmem, ad + 2 * k, bd + 2 * k, p.idesc, (kb | k) != 0);
           }
           umma_commit(&empty[stage]);
-          if (++stage == stages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull[acc]);
+        __syncwarp();
+        ++it_m;
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (leader) umma_commit(&tfull[acc]);
+      if (tracing && leader && it < 100) trace_at(p.trace, 7400 + it);
+      __syncwarp();
     }
-    __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < kEpiW) {
     // ------------------------------------------------------------ epilogue
+    // 16 warps: warp w reads TMEM lanes [32*(w%4), +32) (its quad of rows) and the
+    // contiguous chunk range of column group g = (w-4)/4; one lane = one output row.
     const GemmEpilogue& e = p.e;
-    const int et = threadIdx.x - 128;   // 0..255
-    const int ew = warp - 4;
-    const int quad = warp & 3;          // TMEM lanes [32*quad, 32*quad+32) belong to this warp
-    const int half = ew >> 2;
+    const int et = threadIdx.x;
+    const int ew = warp;
+    const int quad = warp & 3;
+    const int grp = ew >> 2;
     const int nchunk = BN >> 5;
-    const int split = (nchunk + 1) >> 1;
-    const int c_begin = half ? split : 0, c_end = half ? nchunk : split;
+    const int c_begin = (grp * nchunk) / kEpiGroups, c_end = ((grp + 1) * nchunk) / kEpiGroups;
     const int pq = p.P * p.Q;
     const int32_t zp_out = e.zp_out, lo = e.lo, hi = e.hi;
-    const bool out8 = e.out_dtype != DT_S32;
-    const bool is_s8 = e.out_dtype == DT_S8;
-    uint8_t* stage_out = sOut + ew * 2048;
+    constexpr bool out8 = MODE != 2;   // requantize => 8-bit output, raw => int32 (abi guarantees it)
+    const bool tma_st = e.tma_store;
+    uint8_t* stage_base = sOut + ew * 4096;   // double-buffered across tiles
     int sbuf = 0;
+    // staging row pitch = this group's column bytes; swizzle matches the store box (none for 96 B rows)
+    const int row_bytes = (c_end - c_begin) * 32;
+    const uint32_t swz_mask = row_bytes == 128 ? 7u : (row_bytes == 64 ? 3u : (row_bytes == 32 ? 1u : 0u));
+    const CUtensorMap* tmC = grp == 0 ? &tmC0 : (grp == 1 ? &tmC1 : (grp == 2 ? &tmC2 : &tmC3));
+    constexpr int kEpiThreads = 32 * kGemmEpiWarps;
     int cur_n = -1, tile_fast = 1;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
@@ -291,31 +420,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m_blk = t / p.num_n_tiles, n_blk = t - m_blk * p.num_n_tiles;
       if (n_blk != cur_n) {
-        // stage this N-tile's per-column parameters (all 8 epilogue warps)
-        named_bar_sync(1, 32 * kGemmEpiWarps);
+        // stage this N-tile's per-column parameters (all epilogue warps)
+        named_bar_sync(1, kEpiThreads);
         int ok = 1;
-        for (int i = et; i < BN; i += 32 * kGemmEpiWarps) {
+        for (int i = et; i < BN; i += kEpiThreads) {
           const int k = n_blk * BN + i;
-          int4 q = make_int4(0, 0, 0, 0);
+          int32_t M = 0, c = 0, tt = 0;
           if (MODE != 2) {
-            const int32_t M = e.mult[k], r = e.rsh[k];
-            q.z = M;
+            const int32_t r = e.rsh[k];
+            M = e.mult[k];
             if (r >= 33 && r <= 52) {
-              const int tt = r - 32;
-              q.w = tt;
-              q.y = MODE == 0 ? (int32_t)((1u << (tt - 1)) + (uint32_t)zp_out * (1u << tt)) : (int32_t)(1u << (tt - 1));
+              tt = r - 32;
+              c = MODE == 0 ? (int32_t)((1u << (tt - 1)) + (uint32_t)zp_out * (1u << tt)) : (int32_t)(1u << (tt - 1));
             } else {
-              q.w = -r;  // generic 64-bit path
+              tt = -r;  // generic 64-bit path
               ok = 0;
             }
           }
-          sPrm[i] = q;
+          sMT[i] = make_int2(M, tt);
+          sCC[i] = c;
         }
-        for (int i = et; i < ncls * BN; i += 32 * kGemmEpiWarps) {
+        for (int i = et; i < ncls * BN; i += kEpiThreads) {
           const int c = i / BN, j = i - c * BN;
           sOff[c * offp + j] = e.off[(size_t)c * e.Kpad + n_blk * BN + j];
         }
-        tile_fast = named_bar_and(1, 32 * kGemmEpiWarps, ok);
+        tile_fast = named_bar_and(1, kEpiThreads, ok);
         cur_n = n_blk;
       }
       const int row0 = m_blk * kGemmBM + quad * 32;
@@ -331,45 +460,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (e.rowsum) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
       }
+      uint8_t* stage_out = stage_base + sbuf * 2048;
+      if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 4096 + it);
       mbar_wait(&tfull[acc], acc_phase);
+      if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 5120 + it);
+      if (tracing && lane == 0 && it < 100) trace_at(p.trace, 9200 + it * 16 + warp);
       tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
       for (int j = c_begin; j < c_end; ++j) {
         uint32_t v[32];
-        tmem_load32(tmem_base + acc * 256 + j * 32 + ((uint32_t)(quad * 32) << 16), v);
+        if (!(p.dbg & 16)) tmem_load32(tbase + j * 32, v);
         if (j == c_end - 1) {
           // accumulator fully read by this warp: hand the TMEM buffer back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
         }
         const int k0 = n_blk * BN + j * 32;
-        int32_t y[32];
-        const int4* prm = sPrm + j * 32;
-        const int4* offc = reinterpret_cast<const int4*>(sOff + cls * offp + j * 32);
+        const int4* off4 = reinterpret_cast<const int4*>(sOff + cls * offp + j * 32);
+        const int4* mt4 = reinterpret_cast<const int4*>(sMT + j * 32);      // 2 columns per int4
+        const int4* c4 = reinterpret_cast<const int4*>(sCC + j * 32);
+        uint32_t w[8];
+        int32_t y[out8 ? 1 : 32];
         if (tile_fast)
-          requant_row32<MODE, CLAMP, true>(v, prm, offc, rterm, zp_out, lo, hi, y);
+          epi_chunk<MODE, CLAMP, true, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
         else
-          requant_row32<MODE, CLAMP, false>(v, prm, offc, rterm, zp_out, lo, hi, y);
-        if (out8) {
-          uint32_t w[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            w[i] = is_s8 ? pack4_s8(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3])
-                         : pack4_u8(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
-          if (e.tma_store) {
-            // per-warp 32 rows x 32 B sub-tile -> smem -> TMA store (clips rows >= M, cols >= K)
-            uint8_t* buf = stage_out + sbuf * 1024;
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
-            *reinterpret_cast<uint4*>(buf + lane * 32) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4*>(buf + lane * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmC, buf, k0, row0);
-              bulk_commit();
+          epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
+        if (p.dbg & 2) {
+        } else if constexpr (out8) {
+          if (tma_st) {
+            if (j == c_begin) {
+              // the store issued two tiles ago from this buffer must have finished reading it
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
             }
-            sbuf ^= 1;
+            // staged in the TMA swizzle layout of this group's store box
+            const uint32_t l16 = (uint32_t)(lane * row_bytes + (j - c_begin) * 32);
+            const uint32_t s0 = l16 ^ (((l16 >> 7) & swz_mask) << 4);
+            const uint32_t s1 = (l16 + 16) ^ ((((l16 + 16) >> 7) & swz_mask) << 4);
+            *reinterpret_cast<uint4*>(stage_out + s0) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(stage_out + s1) = make_uint4(w[4], w[5], w[6], w[7]);
           } else if (row_ok) {
             uint8_t* o = reinterpret_cast<uint8_t*>(e.out) + (long long)row * e.out_pitch + k0;
             if (k0 + 32 <= p.Nout && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
@@ -386,66 +518,83 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (k0 + 32 <= p.Nout && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<int4*>(o + i) = make_int4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+              *reinterpret_cast<int4*>(o + i) =
+                  make_int4(y[out8 ? 0 : i], y[out8 ? 0 : i + 1], y[out8 ? 0 : i + 2], y[out8 ? 0 : i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (k0 + i < p.Nout) o[i] = y[i];
+              if (k0 + i < p.Nout) o[i] = y[out8 ? 0 : i];
           }
         }
       }
-      if (c_begin == c_end) {  // no columns for this warp (BN == 32): still release the accumulator
+      if (tma_st && c_begin < c_end && !(p.dbg & 2)) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(tmC, stage_out, n_blk * BN + c_begin * 32, row0);
+          bulk_commit();
+        }
+        sbuf ^= 1;
+      }
+      if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 4608 + it);
+      if (tracing && lane == 0 && it < 100) trace_at(p.trace, 10900 + it * 16 + warp);
+      if (c_begin == c_end) {  // no columns for this warp: still release the accumulator
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       }
     }
-    if (e.tma_store && lane == 0) bulk_wait_all();
+    if (tma_st && lane == 0) bulk_wait_all();
     __syncwarp();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (threadIdx.x == 0) trace_at(p.trace, 6002);
+  if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP>
-static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT>
+static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                   const GemmParams& p, int grid, cudaStream_t stream) {
   static int attr_done[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP>;
+  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT>;
   if (dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     if (dev < 64) attr_done[dev] = 1;
   }
-  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1);
+  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb : 0, p.kps);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC, p);
+  kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmParams& p,
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC, const GemmParams& p,
                         int mode, bool clamp, int grid, cudaStream_t stream) {
   const bool cls = p.e.ncls > 1;
-#define QNN_GEMM_CASE(M_, C_, K_) \
-  if (mode == M_ && cls == C_ && clamp == K_) return launch_variant<M_, C_, K_>(tmA, tmB, tmC, p, grid, stream);
-  QNN_GEMM_CASE(0, false, false)
-  QNN_GEMM_CASE(0, false, true)
-  QNN_GEMM_CASE(0, true, false)
-  QNN_GEMM_CASE(0, true, true)
-  QNN_GEMM_CASE(1, false, false)
-  QNN_GEMM_CASE(1, false, true)
-  QNN_GEMM_CASE(1, true, false)
-  QNN_GEMM_CASE(1, true, true)
-  QNN_GEMM_CASE(2, false, false)
-  QNN_GEMM_CASE(2, true, false)
+  const bool s8 = p.e.out_dtype == DT_S8;
+#define QNN_GEMM_CASE(M_, C_, K_, S_)                  \
+  if (mode == M_ && cls == C_ && clamp == K_ && s8 == S_) \
+    return launch_variant<M_, C_, K_, S_>(tmA, tmB, tmC, p, grid, stream);
+#define QNN_GEMM_CASES(M_, C_, K_) QNN_GEMM_CASE(M_, C_, K_, false) QNN_GEMM_CASE(M_, C_, K_, true)
+  QNN_GEMM_CASES(0, false, false)
+  QNN_GEMM_CASES(0, false, true)
+  QNN_GEMM_CASES(0, true, false)
+  QNN_GEMM_CASES(0, true, true)
+  QNN_GEMM_CASES(1, false, false)
+  QNN_GEMM_CASES(1, false, true)
+  QNN_GEMM_CASES(1, true, false)
+  QNN_GEMM_CASES(1, true, true)
+  QNN_GEMM_CASE(2, false, false, false)
+  QNN_GEMM_CASE(2, true, false, false)
+#undef QNN_GEMM_CASES
 #undef QNN_GEMM_CASE
   return cudaErrorInvalidValue;
 }

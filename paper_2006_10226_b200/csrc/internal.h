@@ -41,19 +41,27 @@ struct GemmParams {
   int BK, BN, stages;
   int num_m_tiles, num_n_tiles;
   int im2col;              // 1 => A via im2col TMA over NHWC, 0 => A is a 2-D [M][C] matrix
+  int b_res;               // 1 => all of B resident in smem (single N tile, small weights)
+  int kps;                 // k-blocks per pipeline stage
+  const uint8_t* a_base;   // A operand base (for L2 prefetch), a_pitch bytes per pixel / row
+  long long a_pitch;
+  int H, W, a_halo;        // input geometry for the prefetch range (a_halo = (R-1)*dil_h)
+  int dbg;                 // profiling knobs (QNN_GEMM_DEBUG): 1 no epilogue math, 2 no stores,
+                           // 4 no A loads, 8 no MMAs, 16 no TMEM loads; results are then garbage
+  unsigned long long* trace; // profiling: CTA 0 event timestamps (QNN_GEMM_TRACE), else nullptr
   int P, Q, sh, sw, pt, pl;
   uint32_t idesc;
   GemmEpilogue e;
 };
 
 constexpr int kGemmBM = 128;
-constexpr int kGemmEpiWarps = 8;
+constexpr int kGemmEpiWarps = 16;
 constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls);
-int gemm_max_stages(int BK, int BN, int ncls);
-cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps);
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps);
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
@@ -74,6 +82,8 @@ cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int
                                    cudaStream_t s);
 cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out, int Cp, long long npix, int C,
                                 cudaStream_t s);
+cudaError_t launch_fold_width(const void* in, long long in_cstride, void* out, int N, int H, int W, int C, int Q, int S,
+                              int sw, int pl, int dw, int Cf, cudaStream_t s);
 cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
                               int32_t* pixsum, cudaStream_t s);
 cudaError_t launch_window_sums(const int32_t* pixsum, int N, int H, int W, int P, int Q, int R, int S, int sh,

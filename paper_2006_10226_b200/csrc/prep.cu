@@ -118,6 +118,55 @@ cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out,
   return cudaGetLastError();
 }
 
+// Width fold for small-C convolutions (e.g. the C = 3 stem): X'[n,h,q,j] with
+// j = s*C + c holds A[n, h, q*sw + s*dw - pl, c] (0 outside the image and for
+// j >= S*C), so the R x S conv becomes an R x 1 conv over S*C channels with
+// far fewer, fuller tensor-core K steps.  Zero fill outside the image is
+// corrected by the same border-class offsets as the TMA zero fill (reading R7).
+__global__ void __launch_bounds__(256) fold_width_kernel(const uint8_t* __restrict__ in, long long in_cstride,
+                                                         uint8_t* __restrict__ out, int N, int H, int W, int C, int Q,
+                                                         int S, int sw, int pl, int dw, int Cf) {
+  // one block per input row (n, h): the row is staged in smem with coalesced loads, then
+  // every output pixel q assembles its Cf-byte folded vector and writes it as 16-B stores
+  extern __shared__ uint8_t row[];
+  const long long nh = blockIdx.x;
+  const uint8_t* src = in + nh * W * in_cstride;
+  const int rowbytes = W * C;
+  if (in_cstride == C) {
+    for (int i = threadIdx.x; i < rowbytes; i += blockDim.x) row[i] = src[i];
+  } else {
+    for (int i = threadIdx.x; i < rowbytes; i += blockDim.x) row[i] = src[(long long)(i / C) * in_cstride + i % C];
+  }
+  __syncthreads();
+  const int sc = S * C;
+  const int pieces = Cf / 16;
+  uint8_t* dst = out + nh * (long long)Q * Cf;
+  for (int i = threadIdx.x; i < Q * pieces; i += blockDim.x) {
+    const int q = i / pieces, pc = i - q * pieces;
+    uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const int j = pc * 16 + b;
+      if (j < sc) {
+        const int s = j / C, c = j - s * C;
+        const int w = q * sw + s * dw - pl;
+        if (w >= 0 && w < W) wv[b >> 2] |= (uint32_t)row[w * C + c] << (8 * (b & 3));
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + (long long)q * Cf + pc * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+cudaError_t launch_fold_width(const void* in, long long in_cstride, void* out, int N, int H, int W, int C, int Q, int S,
+                              int sw, int pl, int dw, int Cf, cudaStream_t s) {
+  const size_t smem = (size_t)W * C;
+  if (smem > 48 * 1024) return cudaErrorInvalidValue;
+  fold_width_kernel<<<(unsigned)((long long)N * H), 256, smem, s>>>((const uint8_t*)in, in_cstride, (uint8_t*)out, N,
+                                                                     H, W, C, Q, S, sw, pl, dw, Cf);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Term 3, step 1: per-pixel channel sums (one warp-cooperative pass over A).
 __global__ void pixel_sums_kernel(const uint8_t* __restrict__ in, int a_signed, long long in_cstride, int C,
                                   long long npix, int32_t* __restrict__ pixsum) {

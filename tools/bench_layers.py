@@ -40,18 +40,32 @@ def peaks():
 
 
 class Timer:
-    def __init__(self, flush_mb=256):
-        self.flush = torch.empty(flush_mb * 2 ** 20, dtype=torch.uint8, device="cuda")
+    """Times one op as a CUDA-graph replay so host-side launch preparation (plan,
+    tensor-map encoding, ctypes) never shows up as GPU time.  L2 is flushed before
+    every rep by READING a 512 MB buffer (a write-based flush would leave ~126 MB
+    of dirty lines whose write-back lands inside the timed op)."""
+
+    def __init__(self, flush_mb=512):
+        self.flush = torch.ones(flush_mb * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
 
     def time(self, fn, reps=10, warmup=3):
-        for _ in range(warmup):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
             fn()
         ts = []
         for _ in range(reps):
-            self.flush.fill_(1)
+            torch.sum(self.flush, dim=0, out=self.sink)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            fn()
+            g.replay()
             b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b))
