@@ -312,7 +312,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   // ------------------------------------------------------------ tensor-core plan
   const bool tma_pitch_ok = (pl.in_cs % 16) == 0;
   pl.gW = d->W; pl.gS = d->S; pl.g_sw = d->stride_w; pl.g_pl = d->pad_l; pl.g_pr = d->pad_r; pl.g_dw = d->dil_w;
-  pl.fold = (!tma_pitch_ok || d->C < 16) && d->S > 1 && d->S * d->C <= 128 && (long long)d->W * d->C <= 48 * 1024;
+  pl.fold = (!tma_pitch_ok || d->C < 16) && d->S > 1 && d->S * d->C <= 128;
   if (pl.fold) {
     // X'[n, h, q, s*C + c] = A[n, h, q*sw + s*dw - pl, c] (0 outside): an R x 1 conv over X'
     pl.Ct = round_up(d->S * d->C, 16);

@@ -126,43 +126,71 @@ cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out,
 __global__ void __launch_bounds__(256) fold_width_kernel(const uint8_t* __restrict__ in, long long in_cstride,
                                                          uint8_t* __restrict__ out, int N, int H, int W, int C, int Q,
                                                          int S, int sw, int pl, int dw, int Cf) {
-  // one block per input row (n, h): the row is staged in smem with coalesced loads, then
-  // every output pixel q assembles its Cf-byte folded vector and writes it as 16-B stores
-  extern __shared__ uint8_t row[];
-  const long long nh = blockIdx.x;
-  const uint8_t* src = in + nh * W * in_cstride;
-  const int rowbytes = W * C;
-  if (in_cstride == C) {
-    for (int i = threadIdx.x; i < rowbytes; i += blockDim.x) row[i] = src[i];
-  } else {
-    for (int i = threadIdx.x; i < rowbytes; i += blockDim.x) row[i] = src[(long long)(i / C) * in_cstride + i % C];
+  // one thread per 16-byte piece of a folded pixel; interior windows of a dense row read
+  // their S*C contiguous bytes as aligned 32-bit words (L1-cached, neighbours overlap) and
+  // funnel-shift them into place; border windows fall back to per-byte gathers
+  __shared__ int tab_s[128], tab_c[128];   // folded channel j -> filter column s*dw (or a sentinel), channel c
+  const int sc = S * C;
+  for (int j = threadIdx.x; j < Cf; j += blockDim.x) {
+    const int s = j / C;
+    tab_s[j] = j < sc ? s * dw : -(1 << 20);
+    tab_c[j] = j - s * C;
   }
   __syncthreads();
-  const int sc = S * C;
   const int pieces = Cf / 16;
-  uint8_t* dst = out + nh * (long long)Q * Cf;
-  for (int i = threadIdx.x; i < Q * pieces; i += blockDim.x) {
-    const int q = i / pieces, pc = i - q * pieces;
+  const bool dense = in_cstride == C && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && ((W * C) & 3) == 0 && dw == 1;
+  // 32-bit index arithmetic (the launcher guarantees N*H*Q*pieces < 2^31): 64-bit
+  // division would dominate this bandwidth-bound kernel
+  const uint32_t total = (uint32_t)((long long)N * H * Q * pieces);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t32 = i / (uint32_t)pieces;
+    const int pc = (int)(i - t32 * (uint32_t)pieces);
+    const uint32_t nh32 = t32 / (uint32_t)Q;
+    const int q = (int)(t32 - nh32 * (uint32_t)Q);
+    const long long t = t32, nh = nh32;
+    const int w0 = q * sw - pl;
+    const uint8_t* rowp = in + nh * W * in_cstride;
     uint32_t wv[4] = {0, 0, 0, 0};
+    if (dense && w0 >= 0 && w0 + S <= W) {
+      const int base = w0 * C + pc * 16;
+      const int valid = sc - pc * 16;   // bytes of this piece that are real folded channels
+      if (valid > 0) {
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rowp);
+        const int wa = base >> 2, shb = (base & 3) * 8;
+        const int last = min(W * C / 4 - 1, wa + 4);   // never read past the row
+        uint32_t x[5];
 #pragma unroll
-    for (int b = 0; b < 16; ++b) {
-      const int j = pc * 16 + b;
-      if (j < sc) {
-        const int s = j / C, c = j - s * C;
-        const int w = q * sw + s * dw - pl;
-        if (w >= 0 && w < W) wv[b >> 2] |= (uint32_t)row[w * C + c] << (8 * (b & 3));
+        for (int k = 0; k < 5; ++k) x[k] = __ldg(rw + min(wa + k, last));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wv[k] = shb ? __funnelshift_r(x[k], x[k + 1], shb) : x[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int nb = valid - 4 * k;
+          wv[k] = nb >= 4 ? wv[k] : (nb <= 0 ? 0u : (wv[k] & ((1u << (8 * nb)) - 1u)));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int j = pc * 16 + b;
+        const int w = w0 + tab_s[j];
+        if (w >= 0 && w < W) wv[b >> 2] |= (uint32_t)rowp[(long long)w * in_cstride + tab_c[j]] << (8 * (b & 3));
       }
     }
-    *reinterpret_cast<uint4*>(dst + (long long)q * Cf + pc * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    *reinterpret_cast<uint4*>(out + t * Cf + pc * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
 }
 
 cudaError_t launch_fold_width(const void* in, long long in_cstride, void* out, int N, int H, int W, int C, int Q, int S,
                               int sw, int pl, int dw, int Cf, cudaStream_t s) {
-  const size_t smem = (size_t)W * C;
-  if (smem > 48 * 1024) return cudaErrorInvalidValue;
-  fold_width_kernel<<<(unsigned)((long long)N * H), 256, smem, s>>>((const uint8_t*)in, in_cstride, (uint8_t*)out, N,
-                                                                     H, W, C, Q, S, sw, pl, dw, Cf);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long total = (long long)N * H * Q * (Cf / 16);
+  if (total >= (1LL << 31)) return cudaErrorInvalidValue;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)sms * 16));
+  fold_width_kernel<<<grid, 256, 0, s>>>((const uint8_t*)in, in_cstride, (uint8_t*)out, N, H, W, C, Q, S, sw, pl, dw,
+                                         Cf);
   count_launch();
   return cudaGetLastError();
 }
