@@ -264,6 +264,8 @@ def main():
 
     import torch
     import torch.distributed as dist
+
+    from paper_2006_10226_b200.sharding import max_over_ranks
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -292,11 +294,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(t0.elapsed_time(t1), dist if world > 1 else None, dev)
     ms_per_step = ms / args.steps
     images = args.batch * world * args.steps
     value = images / (ms / 1000.0)
@@ -317,11 +315,7 @@ def main():
         host_out.copy_(net.logits, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([ems], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ems = float(tt.item())
+    ems = max_over_ranks(e0.elapsed_time(e1), dist if world > 1 else None, dev)
     e2e_value = args.batch * world * e2e_steps / (ems / 1000.0)
     h2d = host_in.numel() * 4
     d2h = host_out.numel() * 4

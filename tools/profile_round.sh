@@ -1,0 +1,14 @@
+#!/bin/bash
+# Round profiling (run under gpurun): plain bench, ncu launch list of the same command, one
+# ncu --set full capture of the top GEMM launch (a ResNet-50 b256 layer) and of depthwise.
+set -u
+OUT=gpurun_out
+python bench.py --steps 20 --warmup 3 > $OUT/bench_plain.log 2>&1; echo "bench rc=$?"
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline --breakdown-steps 1 > $OUT/bench_ncu_plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -c 600 --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --breakdown-steps 1 \
+  > $OUT/ncu_launches.log 2>&1; echo "launches rc=$?"
+python tools/bench_layers.py --suite resnet50 --batch 256 --only layer1.0.conv3 --reps 3 > $OUT/top_plain.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:qnn_gemm -s 3 -c 1 -o $OUT/prof_top \
+  python tools/bench_layers.py --suite resnet50 --batch 256 --only layer1.0.conv3 --reps 3 > $OUT/ncu_top.log 2>&1
+echo "top rc=$?"
