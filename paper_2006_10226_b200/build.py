@@ -14,6 +14,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+# extra defines for profiling builds, e.g. QNN_BUILD_DEFS=-DQNN_GEMM_INSTRUMENT (QNN_GEMM_DEBUG /
+# QNN_GEMM_TRACE knobs); rebuild with --force when changing them
+FLAGS += os.environ.get("QNN_BUILD_DEFS", "").split()
 
 
 def _stale() -> bool:

@@ -188,7 +188,7 @@ struct ConvPlan {
   int mode = 0;
   qnn_dtype_t out_dt = QNN_S32;
   // packed blob layout
-  size_t pk_w = 0, pk_off = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
+  size_t pk_w = 0, pk_off = 0, pk_off64 = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
   // workspace layout
   size_t ws_pad = 0, ws_pixsum = 0, ws_rowsum = 0, ws_total = 0;
 };
@@ -372,6 +372,8 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
   pl.pk_off = off;
   off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
+  pl.pk_off64 = off;
+  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 8);
   pl.pk_mult = off;
   off = align256(off + (size_t)pl.Kpad * 4);
   pl.pk_rsh = off;
@@ -439,7 +441,8 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
       e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
-                            pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off), pl.Kpad, s);
+                            pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off),
+                            reinterpret_cast<int64_t*>(pk + pl.pk_off64), pl.Kpad, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = cudaMemcpyAsync(pk + pl.pk_rowcls, pl.rowcls.data(), pl.rowcls.size(), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
@@ -584,6 +587,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8, kGemmBM, pl.BN);
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
+  ep.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
   ep.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
   ep.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
   const bool one_class = pl.ct.ncr * pl.ct.ncc == 1;

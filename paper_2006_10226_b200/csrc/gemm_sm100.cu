@@ -9,21 +9,23 @@
 // (tcgen05.mma.kind::i8, int32 accumulators in TMEM), operands staged by TMA
 // (im2col mode for convolutions: zero fill outside the image, corrected by the
 // per-border-class offsets), a persistent tile loop, and warp specialisation:
-//   warp 0      : TMA producer (one elected lane)
-//   warp 1      : MMA issuer   (one elected lane)
-//   warp 2      : TMEM allocator
-//   warps 4..11 : epilogue (TMEM -> registers -> requantize -> smem -> TMA store)
+//   warps 0..15 : epilogue (TMEM -> registers -> requantize -> smem -> TMA store)
+//   warp 17     : TMEM allocator
+//   warp 18     : TMA producer (one elected lane issues)
+//   warp 19     : MMA issuer   (one elected lane issues)
 // The TMEM accumulator is double-buffered (2 x 256 columns) so the epilogue of
 // tile i overlaps the MMAs of tile i+1.
 //
-// Epilogue cost per output (fast path, rsh = 31 - shift in [33, 52]):
-//   UPWARD: y = (mulhi(v, M) + (2^(t-1) + zp_out*2^t)) >> t,  t = rsh - 32
-// which equals floor(v*M/2^rsh + 1/2) + zp_out exactly: writing v*M = hi*2^32 + lo
-// with 0 <= lo < 2^32, floor((hi*2^32 + lo + 2^(rsh-1))/2^rsh) =
-// floor((hi + 2^(t-1) + lo/2^32)/2^t) = floor((hi + 2^(t-1))/2^t) because the
+// Epilogue cost per output (fast path, rsh = 31 - shift in [33, 52], t = rsh - 32):
+//   UPWARD: y = hi32((v - rterm)*M + K) >> t,   K = off*M + (2^(t-1) + zp_out*2^t)*2^32
+// (one IMAD.WIDE + one SHF).  This equals floor(x*M/2^rsh + 1/2) + zp_out for the
+// exact x = v + off - rterm: with x*M = hi*2^32 + lo, 0 <= lo < 2^32,
+// floor((hi*2^32 + lo + 2^(rsh-1))/2^rsh) = floor((hi + 2^(t-1))/2^t) because the
 // integer hi + 2^(t-1) cannot cross a multiple of 2^t by adding a fraction < 1.
-// Saturation to u8/s8 is done by cvt.pack.sat.  Per-column (M, c, t, off) are
-// staged once per N-tile in shared memory and read as one broadcast LDS.128.
+// K is formed from the exact (int64) offset, and int64 arithmetic is modular, so
+// the sum is exact whenever x fits in int32 (reading R10).  Saturation to u8/s8
+// is done by cvt.pack.sat.  Per-column {M, t} and per-(class, column) K are staged
+// once per N-tile in shared memory and read as broadcast LDS.128 (two columns each).
 #include "common.cuh"
 #include "internal.h"
 
@@ -31,10 +33,17 @@ namespace qnn {
 
 constexpr int kEpiGroups = kGemmEpiWarps / 4;             // column groups (4 warps each cover the 128 rows)
 constexpr int kStageOutBytes = kGemmEpiWarps * 4 * 1024;  // per-warp 2 x (32 rows x <= 64 B) output staging
-constexpr int kParamBytes = 256 * 8 + 256 * 8;            // per-column {M, t} and (c << 32)
+constexpr int kParamBytes = 256 * 8 + 256 * 8;            // per-column {M, t} and c
 
-// per-class offset rows in smem: pitch BN + 4 ints keeps rows 16-B aligned and spreads banks
-static __host__ __device__ inline size_t off_table_bytes(int ncls, int BN) { return (size_t)ncls * (BN + 4) * 4; }
+// per-class offset rows in smem: int64 K (UPWARD) or int32 off (TONEAREST / raw), pitch BN + 4
+// entries: rows stay 16-B aligned and consecutive classes start in different banks
+static __host__ __device__ inline size_t off_table_bytes(int ncls, int BN) { return (size_t)ncls * (BN + 4) * 8; }
+
+#ifdef QNN_GEMM_INSTRUMENT
+constexpr bool kInstrument = true;    // QNN_GEMM_DEBUG knobs and QNN_GEMM_TRACE timestamps compiled in
+#else
+constexpr bool kInstrument = false;
+#endif
 
 // b_res_kb > 0: the whole B operand (b_res_kb k-blocks) stays resident in smem and
 // the pipeline stages carry A only.
@@ -198,6 +207,39 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const int4* _
   }
 }
 
+// UPWARD fast path for one 32-column chunk of one row (see the header): two
+// columns per LDS.128 of {M, t} pairs and per LDS.128 of K values.
+template <bool CLAMP, bool S8OUT, bool RT>
+__device__ __forceinline__ void epi_chunk_up(const uint32_t (&v)[32], const int4* __restrict__ mt4,
+                                             const longlong2* __restrict__ k2, int32_t rterm, int32_t lo,
+                                             int32_t hi, uint32_t (&w)[8]) {
+#pragma unroll
+  for (int q4 = 0; q4 < 8; ++q4) {
+    int32_t yy[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int4 mt = mt4[q4 * 2 + h];
+      const longlong2 kk = k2[q4 * 2 + h];
+      int32_t v0 = (int32_t)v[q4 * 4 + 2 * h], v1 = (int32_t)v[q4 * 4 + 2 * h + 1];
+      if (RT) {  // exact: sum_c A*(W - zp_W) is bounded by R10
+        v0 -= rterm;
+        v1 -= rterm;
+      }
+      const unsigned long long p0 = (unsigned long long)((long long)v0 * mt.x) + (unsigned long long)kk.x;
+      const unsigned long long p1 = (unsigned long long)((long long)v1 * mt.z) + (unsigned long long)kk.y;
+      int32_t r0 = (int32_t)(p0 >> 32) >> mt.y;
+      int32_t r1 = (int32_t)(p1 >> 32) >> mt.w;
+      if (CLAMP) {
+        r0 = min(max(r0, lo), hi);
+        r1 = min(max(r1, lo), hi);
+      }
+      yy[2 * h] = r0;
+      yy[2 * h + 1] = r1;
+    }
+    w[q4] = S8OUT ? pack4_s8(yy[0], yy[1], yy[2], yy[3]) : pack4_u8(yy[0], yy[1], yy[2], yy[3]);
+  }
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -209,7 +251,7 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
-  if (tr && blockIdx.x == 0) tr[slot] = clock64();
+  if (kInstrument && tr && blockIdx.x == 0) tr[slot] = clock64();
 }
 
 template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT>
@@ -228,7 +270,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * kps * a_bytes;   // ring of B stages, or the resident B (num_kb blocks)
   uint8_t* sOut = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);
-  const bool tracing = p.trace != nullptr && blockIdx.x == 0;
+  const bool tracing = kInstrument && p.trace != nullptr && blockIdx.x == 0;
+  const int dbg = kInstrument ? p.dbg : 0;
   int2* sMT = reinterpret_cast<int2*>(sOut + kStageOutBytes);          // {M, t} per column
   int32_t* sCC = reinterpret_cast<int32_t*>(sMT + 256);               // c per column
   int32_t* sOff = sCC + 512;
@@ -268,15 +311,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     mbar_init(bres_full, 1);
     fence_mbar_init();
   }
-  if (threadIdx.x == 0) trace_at(p.trace, 6000);
+  if (tracing && threadIdx.x == 0) trace_at(p.trace, 6000);
   if (warp == kAllocWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) trace_at(p.trace, 6001);
+  if (tracing && threadIdx.x == 0) trace_at(p.trace, 6001);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  // tile t = m_blk * nn + n_blk, visited t = blockIdx.x, += gridDim.x: (m_blk, n_blk) advanced without division
+  const int nn = p.num_n_tiles;
+  const int m_first = blockIdx.x / nn, n_first = blockIdx.x - m_first * nn;
+  const int m_step = gridDim.x / nn, n_step = gridDim.x - m_step * nn;
+#define QNN_NEXT_TILE()  \
+  do {                   \
+    n_blk += n_step;     \
+    m_blk += m_step;     \
+    if (n_blk >= nn) {   \
+      n_blk -= nn;       \
+      ++m_blk;           \
+    }                    \
+  } while (0)
 
   if (warp == kProdWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -293,9 +349,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     int stage = 0, it_p = 0;
     uint32_t phase = 0;
-    const bool skip_a = p.dbg & 4;
+    const bool skip_a = dbg & 4;
+    int m_blk = m_first, n_blk = n_first;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m_blk = t / p.num_n_tiles, n_blk = t - m_blk * p.num_n_tiles;
       const int m0 = m_blk * kGemmBM;
       int an = 0, ah = 0, aw = 0;
       if (p.im2col) {
@@ -344,6 +400,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           phase ^= 1;
         }
       }
+      QNN_NEXT_TILE();
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
@@ -354,7 +411,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int it = 0;
     const uint64_t adesc0 = make_sdesc(smem_u32(sA), BK);
     const uint64_t bdesc0 = make_sdesc(smem_u32(sB), BK);
-    const int ksteps = (p.dbg & 8) ? 0 : BK / 32;
+    const int ksteps = (dbg & 8) ? 0 : BK / 32;
     if (b_res) mbar_wait(bres_full, 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -414,11 +471,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const CUtensorMap* tmC = grp == 0 ? &tmC0 : (grp == 1 ? &tmC1 : (grp == 2 ? &tmC2 : &tmC3));
     constexpr int kEpiThreads = 32 * kGemmEpiWarps;
     int cur_n = -1, tile_fast = 1;
+    const bool has_rt = e.rowsum != nullptr;
     int it = 0;
+    int m_blk = m_first, n_blk = n_first;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m_blk = t / p.num_n_tiles, n_blk = t - m_blk * p.num_n_tiles;
       if (n_blk != cur_n) {
         // stage this N-tile's per-column parameters (all epilogue warps)
         named_bar_sync(1, kEpiThreads);
@@ -440,9 +498,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           sMT[i] = make_int2(M, tt);
           sCC[i] = c;
         }
-        for (int i = et; i < ncls * BN; i += kEpiThreads) {
-          const int c = i / BN, j = i - c * BN;
-          sOff[c * offp + j] = e.off[(size_t)c * e.Kpad + n_blk * BN + j];
+        if (MODE == 0) {
+          // K[cls][j] = off64*M + c*2^32 (modular int64), fast columns only
+          long long* sK = reinterpret_cast<long long*>(sOff);
+          for (int i = et; i < ncls * BN; i += kEpiThreads) {
+            const int c = i / BN, j = i - c * BN;
+            const int k = n_blk * BN + j;
+            const int32_t r = e.rsh[k];
+            unsigned long long K = 0;
+            if (r >= 33 && r <= 52) {
+              const int tt = r - 32;
+              const unsigned long long c64 =
+                  (1ull << (tt - 1)) + ((unsigned long long)(long long)zp_out << tt);
+              K = (unsigned long long)e.off64[(size_t)c * e.Kpad + k] * (unsigned long long)(long long)e.mult[k] +
+                  (c64 << 32);
+            }
+            sK[c * offp + j] = (long long)K;
+          }
+        } else {
+          for (int i = et; i < ncls * BN; i += kEpiThreads) {
+            const int c = i / BN, j = i - c * BN;
+            sOff[c * offp + j] = e.off[(size_t)c * e.Kpad + n_blk * BN + j];
+          }
         }
         tile_fast = named_bar_and(1, kEpiThreads, ok);
         cur_n = n_blk;
@@ -470,7 +547,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
       for (int j = c_begin; j < c_end; ++j) {
         uint32_t v[32];
-        if (!(p.dbg & 16)) tmem_load32(tbase + j * 32, v);
+        if (!(dbg & 16)) tmem_load32(tbase + j * 32, v);
         if (j == c_end - 1) {
           // accumulator fully read by this warp: hand the TMEM buffer back to the MMA warp
           tc_fence_before();
@@ -479,16 +556,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
         }
         const int k0 = n_blk * BN + j * 32;
-        const int4* off4 = reinterpret_cast<const int4*>(sOff + cls * offp + j * 32);
         const int4* mt4 = reinterpret_cast<const int4*>(sMT + j * 32);      // 2 columns per int4
-        const int4* c4 = reinterpret_cast<const int4*>(sCC + j * 32);
         uint32_t w[8];
         int32_t y[out8 ? 1 : 32];
-        if (tile_fast)
-          epi_chunk<MODE, CLAMP, true, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
-        else
-          epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
-        if (p.dbg & 2) {
+        if (MODE == 0) {
+          if (tile_fast) {
+            const longlong2* k2 = reinterpret_cast<const longlong2*>(reinterpret_cast<const long long*>(sOff) +
+                                                                     cls * offp + j * 32);
+            if (has_rt)
+              epi_chunk_up<CLAMP, S8OUT, true>(v, mt4, k2, rterm, lo, hi, w);
+            else
+              epi_chunk_up<CLAMP, S8OUT, false>(v, mt4, k2, rterm, lo, hi, w);
+          } else {
+            // generic 64-bit rounding (shifts outside [33, 52]): int32 offsets straight from global memory
+            const int4* off4 = reinterpret_cast<const int4*>(e.off + (size_t)cls * e.Kpad + k0);
+            epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, mt4, rterm, zp_out, lo, hi, w, y);
+          }
+        } else {
+          const int4* off4 = reinterpret_cast<const int4*>(sOff + cls * offp + j * 32);
+          const int4* c4 = reinterpret_cast<const int4*>(sCC + j * 32);
+          if (tile_fast)
+            epi_chunk<MODE, CLAMP, true, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
+          else
+            epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
+        }
+        if (dbg & 2) {
         } else if constexpr (out8) {
           if (tma_st) {
             if (j == c_begin) {
@@ -527,7 +619,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      if (tma_st && c_begin < c_end && !(p.dbg & 2)) {
+      if (tma_st && c_begin < c_end && !(dbg & 2)) {
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -543,14 +635,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       }
+      QNN_NEXT_TILE();
     }
     if (tma_st && lane == 0) bulk_wait_all();
     __syncwarp();
   }
 
+#undef QNN_NEXT_TILE
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) trace_at(p.trace, 6002);
+  if (tracing && threadIdx.x == 0) trace_at(p.trace, 6002);
   if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);

@@ -19,7 +19,8 @@ constexpr int kMaxQuantParams = 2048;  // per-channel quantize/dequantize params
 //   reduce  = (r, s, c-chunk) k-blocks of BK bytes,     num_kb = R*S*nchunks
 // ---------------------------------------------------------------------------
 struct GemmEpilogue {
-  const int32_t* off;      // [ncls][Kpad]: bias - zpA*colsum_cls + zpA*zpW*Cg*nvalid_cls
+  const int32_t* off;      // [ncls][Kpad]: bias - zpA*colsum_cls + zpA*zpW*Cg*nvalid_cls (int32 wrap)
+  const int64_t* off64;    // [ncls][Kpad]: the same offsets, exact (folded into the UPWARD fast path)
   const int32_t* mult;     // [Kpad] fixed-point multiplier M_k
   const int32_t* rsh;      // [Kpad] right shift 31 - shift_k (1..62)
   const uint8_t* rowcls;   // [P] row border class (nullptr => class 0)
@@ -76,7 +77,7 @@ struct ClassTable {
 cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad,
                                 cudaStream_t s);
 cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
-                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int Kpad,
+                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int64_t* off64, int Kpad,
                                 cudaStream_t s);
 cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int16_t* Wd, int C, int RS,
                                    cudaStream_t s);

@@ -45,13 +45,14 @@ cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, i
 
 __global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed, const int32_t* __restrict__ bias,
                                     int K, int R, int S, int C, int32_t zpA, int32_t zpW, ClassTable ct,
-                                    int32_t* __restrict__ off, int Kpad) {
+                                    int32_t* __restrict__ off, int64_t* __restrict__ off64, int Kpad) {
   const int ncls = ct.ncr * ct.ncc;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= ncls * Kpad) return;
   const int cls = idx / Kpad, k = idx - cls * Kpad;
   if (k >= K) {
     off[idx] = 0;
+    off64[idx] = 0;
     return;
   }
   const int rc = cls / ct.ncc, cc = cls - rc * ct.ncc;
@@ -68,14 +69,15 @@ __global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed,
   const long long v = (bias ? (long long)bias[k] : 0) - (long long)zpA * colsum +
                       (long long)zpA * zpW * (long long)C * nvalid;
   off[idx] = (int32_t)(uint32_t)(unsigned long long)v;
+  off64[idx] = v;
 }
 
 cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
-                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int Kpad,
-                                cudaStream_t s) {
+                                int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int64_t* off64,
+                                int Kpad, cudaStream_t s) {
   const int total = ct.ncr * ct.ncc * Kpad;
   fold_offsets_kernel<<<(total + 127) / 128, 128, 0, s>>>((const uint8_t*)W, w_signed, bias, K, R, S, C, zpA, zpW,
-                                                         ct, off, Kpad);
+                                                         ct, off, off64, Kpad);
   count_launch();
   return cudaGetLastError();
 }
