@@ -7,7 +7,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libqnn.so")
+LIB = os.environ.get("QNN_LIB_OUT") or os.path.join(PKG, "libqnn.so")
 SOURCES = ["abi.cu", "gemm_sm100.cu", "prep.cu", "depthwise.cu", "elementwise.cu"]
 HEADERS = ["common.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -32,7 +32,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" + os.environ.get("QNN_BUILD_TAG", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -545,7 +545,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   const bool tma_store = !no_tma_store && pl.requant && (pl.out_cs % 16) == 0 &&
                          (reinterpret_cast<uintptr_t>(output) & 15) == 0;
   if (tma_store) {
-    const int nchunk = pl.BN / 32, ng = kGemmEpiWarps / 4;
+    // column groups of one epilogue warp set (gemm_epi_sets): 4 / nsets
+    const int nchunk = pl.BN / 32, ng = 4 / gemm_epi_sets(pl.BN, pl.num_n);
     for (int h = 0; h < ng; ++h) {
       const int width = ((h + 1) * nchunk / ng - h * nchunk / ng) * 32;
       const int wb = width ? width : 32;

@@ -10,9 +10,9 @@
 // (im2col mode for convolutions: zero fill outside the image, corrected by the
 // per-border-class offsets), a persistent tile loop, and warp specialisation:
 //   warps 0..15 : epilogue (TMEM -> registers -> requantize -> smem -> TMA store)
-//   warp 17     : TMEM allocator
 //   warp 18     : TMA producer (one elected lane issues)
-//   warp 19     : MMA issuer   (one elected lane issues)
+//   warp 19     : MMA issuer (one elected lane issues) and TMEM allocator
+// (warps 16 and 17 idle; 640 threads leave 96 registers per thread.)
 // The TMEM accumulator is double-buffered (2 x 256 columns) so the epilogue of
 // tile i overlaps the MMAs of tile i+1.
 //
@@ -31,7 +31,6 @@
 
 namespace qnn {
 
-constexpr int kEpiGroups = kGemmEpiWarps / 4;             // column groups (4 warps each cover the 128 rows)
 constexpr int kStageOutBytes = kGemmEpiWarps * 4 * 1024;  // per-warp 2 x (32 rows x <= 64 B) output staging
 constexpr int kParamBytes = 256 * 8 + 256 * 8;            // per-column {M, t} and c
 
@@ -52,7 +51,7 @@ constexpr bool kInstrument = false;
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps) {
   const size_t a = (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
   const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * b : stages * (a + b * kps);
-  return 1024 + ring + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 256;
+  return 1024 + ring + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
 }
 
 int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps) {
@@ -264,6 +263,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // 1024-B aligned base (SW128 atoms); pointer arithmetic on the __shared__ array keeps the address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int BK = p.BK, BN = p.BN, stages = p.stages;
+  const int nacc = gemm_acc_bufs(BN), acc_log = nacc == 8 ? 3 : (nacc == 4 ? 2 : 1);
+  const uint32_t acc_cols = 512u / nacc;
+  const int nsets = gemm_epi_sets(BN, p.num_n_tiles);
   const uint32_t a_bytes = kGemmBM * BK, b_bytes = BN * BK;
   const bool b_res = p.b_res;
   const int kps = p.kps;                   // k-blocks per pipeline stage
@@ -280,17 +282,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sOff) + off_table_bytes(ncls, BN));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bres_full = tempty + 2;
+  uint64_t* tempty = tfull + 8;
+  uint64_t* bres_full = tempty + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-critical
   // single-thread roles get the highest ids and are never starved by waiting epilogue warps.
   constexpr int kEpiW = kGemmEpiWarps;        // epilogue warps 0..15
-  constexpr int kAllocWarp = kEpiW + 1;       // TMEM allocator
   constexpr int kProdWarp = kEpiW + 2;        // TMA producer
   constexpr int kMmaWarp = kEpiW + 3;         // MMA issuer
+  constexpr int kAllocWarp = kMmaWarp;        // TMEM allocator (the MMA warp, before its loop)
   if (warp == kProdWarp && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -304,9 +306,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < nacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kGemmEpiWarps);
+      mbar_init(&tempty[a], kGemmEpiWarps / nsets);   // every warp of the set that owns the tile
     }
     mbar_init(bres_full, 1);
     fence_mbar_init();
@@ -414,13 +416,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ksteps = (dbg & 8) ? 0 : BK / 32;
     if (b_res) mbar_wait(bres_full, 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = it & (nacc - 1);
+      const uint32_t acc_phase = (it >> acc_log) & 1;
       if (tracing && leader && it < 100) trace_at(p.trace, 7200 + it);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       if (tracing && leader && it < 100) trace_at(p.trace, 7300 + it);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * 256;
+      const uint32_t d_tmem = tmem_base + acc * acc_cols;
       for (int kb0 = 0; kb0 < p.num_kb; kb0 += kps) {
         const int nk = min(kps, p.num_kb - kb0);
         if (tracing && leader && it_m < 256) trace_at(p.trace, 6900 + it_m);
@@ -450,15 +452,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp < kEpiW) {
     // ------------------------------------------------------------ epilogue
-    // 16 warps: warp w reads TMEM lanes [32*(w%4), +32) (its quad of rows) and the
-    // contiguous chunk range of column group g = (w-4)/4; one lane = one output row.
+    // 16 warps in nsets sets taking alternate tiles; within a set, warp w reads TMEM lanes
+    // [32*(w%4), +32) (its quad of rows) and the contiguous chunk range of its column
+    // group; one lane = one output row.
     const GemmEpilogue& e = p.e;
     const int et = threadIdx.x;
     const int ew = warp;
     const int quad = warp & 3;
-    const int grp = ew >> 2;
+    const int wps = kGemmEpiWarps / nsets;        // warps per set
+    const int set = ew / wps;
+    const int ngrp = wps >> 2;                    // column groups per set
+    const int grp = (ew - set * wps) >> 2;
     const int nchunk = BN >> 5;
-    const int c_begin = (grp * nchunk) / kEpiGroups, c_end = ((grp + 1) * nchunk) / kEpiGroups;
+    const int c_begin = (grp * nchunk) / ngrp, c_end = ((grp + 1) * nchunk) / ngrp;
     const int pq = p.P * p.Q;
     const int32_t zp_out = e.zp_out, lo = e.lo, hi = e.hi;
     constexpr bool out8 = MODE != 2;   // requantize => 8-bit output, raw => int32 (abi guarantees it)
@@ -472,17 +478,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int kEpiThreads = 32 * kGemmEpiWarps;
     int cur_n = -1, tile_fast = 1;
     const bool has_rt = e.rowsum != nullptr;
-    int it = 0;
     int m_blk = m_first, n_blk = n_first;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      if (n_blk != cur_n) {
+    if (nsets > 1) {   // single N tile: tile t is (t, 0)
+      m_blk = blockIdx.x + set * gridDim.x;
+      n_blk = 0;
+    }
+    // the first N tile's parameters are staged before the loop by all 16 warps (a set may own
+    // no tile at all); later N-tile changes only happen with one set, where all warps see them
+    for (int t = blockIdx.x + set * gridDim.x, it = set, first = 1; t < num_tiles || first;
+         t += nsets * gridDim.x, it += nsets, first = 0) {
+      const int acc = it & (nacc - 1);
+      const uint32_t acc_phase = (it >> acc_log) & 1;
+      if (first || n_blk != cur_n) {
+        const int nb = first ? n_first : n_blk;
         // stage this N-tile's per-column parameters (all epilogue warps)
         named_bar_sync(1, kEpiThreads);
         int ok = 1;
         for (int i = et; i < BN; i += kEpiThreads) {
-          const int k = n_blk * BN + i;
+          const int k = nb * BN + i;
           int32_t M = 0, c = 0, tt = 0;
           if (MODE != 2) {
             const int32_t r = e.rsh[k];
@@ -503,7 +516,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           long long* sK = reinterpret_cast<long long*>(sOff);
           for (int i = et; i < ncls * BN; i += kEpiThreads) {
             const int c = i / BN, j = i - c * BN;
-            const int k = n_blk * BN + j;
+            const int k = nb * BN + j;
             const int32_t r = e.rsh[k];
             unsigned long long K = 0;
             if (r >= 33 && r <= 52) {
@@ -518,11 +531,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         } else {
           for (int i = et; i < ncls * BN; i += kEpiThreads) {
             const int c = i / BN, j = i - c * BN;
-            sOff[c * offp + j] = e.off[(size_t)c * e.Kpad + n_blk * BN + j];
+            sOff[c * offp + j] = e.off[(size_t)c * e.Kpad + nb * BN + j];
           }
         }
         tile_fast = named_bar_and(1, kEpiThreads, ok);
-        cur_n = n_blk;
+        cur_n = nb;
+        if (t >= num_tiles) break;   // staged for the other sets only
       }
       const int row0 = m_blk * kGemmBM + quad * 32;
       const int row = row0 + lane;
@@ -543,9 +557,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 5120 + it);
       if (tracing && lane == 0 && it < 100) trace_at(p.trace, 9200 + it * 16 + warp);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + acc * 256 + ((uint32_t)(quad * 32) << 16);
+      const uint32_t tbase = tmem_base + acc * acc_cols + ((uint32_t)(quad * 32) << 16);
+      // common case (UPWARD fast path, TMA store, two chunks per warp): both TMEM loads in
+      // flight at once and the accumulator released before any math
+#ifdef QNN_EPI_NO_TWO
+      const bool two = false;
+#else
+      const bool two = MODE == 0 && tile_fast && tma_st && !dbg && c_end - c_begin == 2;
+#endif
+      if (two) {
+        uint32_t va[32], vb[32];
+        tmem_ld32_nowait(tbase + c_begin * 32, va);
+        tmem_ld32_nowait(tbase + c_begin * 32 + 32, vb);
+        tmem_wait32(va);
+        tmem_wait32(vb);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        const long long* kbase = reinterpret_cast<const long long*>(sOff) + cls * offp + c_begin * 32;
+        const int4* mt4 = reinterpret_cast<const int4*>(sMT + c_begin * 32);
+        uint32_t w[8];
+        const uint32_t l16 = (uint32_t)(lane * 64);   // 64-B staging rows, 128-B swizzle atoms
+        const uint32_t sw = ((l16 >> 7) & 3u) << 4;
+        if (has_rt)
+          epi_chunk_up<CLAMP, S8OUT, true>(va, mt4, reinterpret_cast<const longlong2*>(kbase), rterm, lo, hi, w);
+        else
+          epi_chunk_up<CLAMP, S8OUT, false>(va, mt4, reinterpret_cast<const longlong2*>(kbase), rterm, lo, hi, w);
+        *reinterpret_cast<uint4*>(stage_out + (l16 ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(stage_out + ((l16 + 16) ^ sw)) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (has_rt)
+          epi_chunk_up<CLAMP, S8OUT, true>(vb, mt4 + 16, reinterpret_cast<const longlong2*>(kbase + 32), rterm, lo,
+                                           hi, w);
+        else
+          epi_chunk_up<CLAMP, S8OUT, false>(vb, mt4 + 16, reinterpret_cast<const longlong2*>(kbase + 32), rterm, lo,
+                                            hi, w);
+        *reinterpret_cast<uint4*>(stage_out + ((l16 + 32) ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(stage_out + ((l16 + 48) ^ sw)) = make_uint4(w[4], w[5], w[6], w[7]);
+      }
 #pragma unroll 1
-      for (int j = c_begin; j < c_end; ++j) {
+      for (int j = two ? c_end : c_begin; j < c_end; ++j) {
         uint32_t v[32];
         if (!(dbg & 16)) tmem_load32(tbase + j * 32, v);
         if (j == c_end - 1) {
@@ -635,7 +688,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       }
-      QNN_NEXT_TILE();
+      if (nsets > 1)
+        m_blk += nsets * gridDim.x;
+      else
+        QNN_NEXT_TILE();
     }
     if (tma_st && lane == 0) bulk_wait_all();
     __syncwarp();

@@ -57,7 +57,23 @@ struct GemmParams {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmEpiWarps = 16;
-constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
+constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;  // + one warpgroup: producer, MMA/allocator, 2 idle
+
+// TMEM accumulator buffers: 512 columns split into the largest power-of-two count
+// (<= 8) of buffers at least BN wide, so narrow tiles keep more tiles in flight.
+__host__ __device__ inline int gemm_acc_bufs(int BN) {
+  int n = 8;
+  while (n > 2 && 512 / n < BN) n >>= 1;
+  return n;
+}
+// Epilogue warp sets: with fewer than four 32-column chunks per tile and a single N
+// tile, the 16 epilogue warps split into sets that take alternate tiles (each set
+// still covers all 128 rows: 4 quads x 4/nsets column groups).
+__host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles) {
+  const int nchunk = BN / 32;
+  if (num_n_tiles != 1 || nchunk >= 3) return 1;
+  return 4 / nchunk;   // 1 chunk -> 4 sets, 2 chunks -> 2 sets
+}
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps);

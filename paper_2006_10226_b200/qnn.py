@@ -15,7 +15,8 @@ from typing import Sequence
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libqnn.so")
+# QNN_LIB: load an alternative in-tree build (A/B experiments); defaults to the package's libqnn.so
+LIB_PATH = os.environ.get("QNN_LIB") or os.path.join(_PKG, "libqnn.so")
 _lock = threading.Lock()
 _lib = None
 
