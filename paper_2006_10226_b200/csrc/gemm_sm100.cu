@@ -217,8 +217,13 @@ __device__ __forceinline__ void epi_chunk_up(const uint32_t (&v)[32], const int4
     int32_t yy[4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+#ifdef QNN_EXP_NOLDS
+      const int4 mt = mt4[0];
+      const longlong2 kk = k2[0];
+#else
       const int4 mt = mt4[q4 * 2 + h];
       const longlong2 kk = k2[q4 * 2 + h];
+#endif
       int32_t v0 = (int32_t)v[q4 * 4 + 2 * h], v1 = (int32_t)v[q4 * 4 + 2 * h + 1];
       if (RT) {  // exact: sum_c A*(W - zp_W) is bounded by R10
         v0 -= rterm;

@@ -111,3 +111,75 @@ def test_empty_tensor(q):
     x = torch.empty(0, dtype=torch.int32, device="cuda")
     y = q.qnn_requantize(x, [1.0], 0, 1.0, 0, "u8")
     assert y.numel() == 0
+
+
+# ---- fast-path coverage: per-tensor int32 with zp_in == 0, and the two vectorised
+# per-channel layouts (channel = fastest axis with C % 16 == 0; inner extent % 16 == 0)
+FAST_LAYOUTS = [((3, 7, 9, 64), -1), ((2, 5, 11, 48), 3), ((4, 24, 8, 8), 1), ((2, 3, 16, 5), 1),
+                ((2, 7, 3, 4), 1), ((5, 33, 129), 1)]
+
+
+@pytest.mark.parametrize("in_dt", ["s32", "u8", "s8"])
+@pytest.mark.parametrize("mode", ["upward", "tonearest"])
+def test_requantize_fast_layouts(q, in_dt, mode):
+    g = np.random.default_rng(zlib.crc32(f"fast{in_dt}{mode}".encode()))
+    for shape, axis in FAST_LAYOUTS + [((40000,), -1)]:
+        x = _rand(g, shape, in_dt)
+        flat = x.reshape(-1)
+        if in_dt == "s32":
+            flat[:3] = [-2 ** 31, 2 ** 31 - 1, 0]
+        C = shape[axis] if len(shape) > 1 else 1
+        lo, hi = (1e-4, 1e-2) if in_dt == "s32" else (0.05, 2.0)
+        sc = g.uniform(lo, hi, size=C).astype(np.float32)
+        zi = 0 if in_dt == "s32" else int(g.integers(-128, 128) if in_dt == "s8" else g.integers(0, 256))
+        for out_dt, zo in (("u8", 7), ("s8", -3), ("s32", 0)):
+            want = orc.requantize(x, sc, zi, 0.7, zo, out_dt, mode, axis=axis)
+            got = q.qnn_requantize(torch.from_numpy(x).cuda(), sc, zi, 0.7, zo, out_dt, mode,
+                                   axis=axis).cpu().numpy()
+            assert np.array_equal(got, want), (shape, axis, out_dt, np.argwhere(got != want)[:5])
+
+
+@pytest.mark.parametrize("out_dt", ["u8", "s8"])
+def test_quantize_fast_layouts(q, out_dt):
+    g = np.random.default_rng(21)
+    for shape, axis in FAST_LAYOUTS:
+        x = (g.standard_normal(shape) * 3).astype(np.float32)
+        x.reshape(-1)[:5] = [np.nan, np.inf, -np.inf, 0.0, 1e30]
+        C = shape[axis]
+        sc = g.uniform(0.01, 0.1, size=C).astype(np.float32)
+        zp = g.integers(0, 256, size=C) if out_dt == "u8" else g.integers(-128, 128, size=C)
+        want = orc.quantize(x, sc, zp, out_dt, axis)
+        got = q.qnn_quantize(torch.from_numpy(x).cuda(), sc, zp, out_dt, axis).cpu().numpy()
+        assert np.array_equal(got, want), (shape, axis)
+
+
+@pytest.mark.parametrize("in_dt", ["u8", "s8"])
+def test_dequantize_fast_layouts(q, in_dt):
+    g = np.random.default_rng(23)
+    for shape, axis in FAST_LAYOUTS:
+        x = _rand(g, shape, in_dt)
+        C = shape[axis]
+        sc = g.uniform(1e-4, 0.1, size=C).astype(np.float32)
+        zp = g.integers(0, 256, size=C) if in_dt == "u8" else g.integers(-128, 128, size=C)
+        want = orc.dequantize(x, sc, zp, axis)
+        got = q.qnn_dequantize(torch.from_numpy(x).cuda(), sc, zp, axis).cpu().numpy()
+        assert np.array_equal(got.view(np.int32), want.view(np.int32)), (shape, axis)
+
+
+def test_quantize_division_is_ieee_on_hard_cases(q):
+    """The fast quantize divides via a Markstein-corrected reciprocal; it must equal the
+    oracle's IEEE x / s on values that sit at or next to half-integers of x / s, and on
+    awkward divisors (all-ones mantissas, powers of two, tiny/huge scales)."""
+    g = np.random.default_rng(31)
+    scales = np.array([np.float32(v) for v in (1.0, 0.5, 3.0, 0.1, 1 / 3, 0.0078125, 1e-30, 1e30)] +
+                      [np.nextafter(np.float32(2.0), np.float32(0)), np.nextafter(np.float32(1.0), np.float32(0))] +
+                      list(g.uniform(1e-3, 10, 6).astype(np.float32)), dtype=np.float32)
+    for s in scales:
+        k = np.arange(-300, 301, dtype=np.float64) + 0.5
+        base = (k * np.float64(s)).astype(np.float32)
+        near = np.concatenate([base, np.nextafter(base, np.float32(np.inf)), np.nextafter(base, np.float32(-np.inf)),
+                               (g.standard_normal(200000) * 200 * np.float64(s)).astype(np.float32)])
+        x = near.astype(np.float32)
+        want = orc.quantize(x, [s], [128], "u8", -1)
+        got = q.qnn_quantize(torch.from_numpy(x).cuda(), [float(s)], [128], "u8", -1).cpu().numpy()
+        assert np.array_equal(got, want), (float(s), np.argwhere(got != want)[:5])
