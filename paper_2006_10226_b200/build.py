@@ -8,8 +8,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.environ.get("QNN_LIB_OUT") or os.path.join(PKG, "libqnn.so")
-SOURCES = ["abi.cu", "gemm_sm100.cu", "prep.cu", "depthwise.cu", "elementwise.cu"]
-HEADERS = ["common.cuh", "internal.h"]
+SOURCES = ["abi.cu", "gemm_sm100.cu", "prep.cu", "depthwise.cu", "depthwise_tc.cu", "elementwise.cu"]
+HEADERS = ["common.cuh", "epilogue.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",

@@ -169,6 +169,7 @@ static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 // ---------------------------------------------------------------------------
 struct ConvPlan {
   bool depthwise = false;
+  bool dwtc = false;       // depthwise on the tensor cores (weights packed for it)
   int P = 0, Q = 0;
   long long M = 0;
   int in_cs = 0, out_cs = 0;
@@ -188,7 +189,7 @@ struct ConvPlan {
   int mode = 0;
   qnn_dtype_t out_dt = QNN_S32;
   // packed blob layout
-  size_t pk_w = 0, pk_off = 0, pk_off64 = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
+  size_t pk_w = 0, pk_off = 0, pk_off64 = 0, pk_dwtc_w = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
   // workspace layout
   size_t ws_pad = 0, ws_pixsum = 0, ws_rowsum = 0, ws_total = 0;
 };
@@ -301,9 +302,35 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     pl.pk_bias = off;
     off = align256(off + (size_t)C * 4);
     pl.pk_mult = off;
-    off = align256(off + (size_t)C * 4);
+    off = align256(off + (size_t)(C + 31) / 32 * 32 * 4);
     pl.pk_rsh = off;
-    off = align256(off + (size_t)C * 4);
+    off = align256(off + (size_t)(C + 31) / 32 * 32 * 4);
+    // tensor-core path (depthwise_tc.cu): diagonal B tiles, per-border-class folded offsets
+    pl.dwtc = C % 16 == 0 && d->kernel_dtype == QNN_S8 && d->kernel_zero_point == 0 && d->dil_h == 1 &&
+              d->dil_w == 1 && (d->stride_h == 1 || d->stride_h == 2) && (d->stride_w == 1 || d->stride_w == 2) &&
+              pl.in_cs % 16 == 0 && pl.out_cs % 16 == 0;
+    if (pl.dwtc) {
+      if (build_classes(pl.P, d->H, d->R, d->stride_h, d->pad_t, d->dil_h, pl.ct.r_lo, pl.ct.r_hi, &pl.ct.ncr,
+                        pl.rowcls) != QNN_OK ||
+          build_classes(pl.Q, d->W, d->S, d->stride_w, d->pad_l, d->dil_w, pl.ct.s_lo, pl.ct.s_hi, &pl.ct.ncc,
+                        pl.colcls) != QNN_OK ||
+          pl.ct.ncr * pl.ct.ncc > 64)
+        pl.dwtc = false;
+    }
+    if (pl.dwtc) {
+      const int Cpad = (C + 31) / 32 * 32, ncls = pl.ct.ncr * pl.ct.ncc;
+      pl.Kpad = Cpad;
+      pl.pk_dwtc_w = off;
+      off = align256(off + (size_t)RS * Cpad * 32);
+      pl.pk_off = off;
+      off = align256(off + (size_t)ncls * Cpad * 4);
+      pl.pk_off64 = off;
+      off = align256(off + (size_t)ncls * Cpad * 8);
+      pl.pk_rowcls = off;
+      off = align256(off + (size_t)pl.P);
+      pl.pk_colcls = off;
+      off = align256(off + (size_t)pl.Q);
+    }
     pl.pk_total = off;
     pl.ws_total = 0;
     return QNN_OK;
@@ -413,7 +440,7 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
   const int w_signed = d->kernel_dtype == QNN_S8;
 
   // per-channel multipliers m_k = s_A * s_W[k] / s_out (reading R3)
-  const int nmult = pl.depthwise ? d->C : pl.Kpad;
+  const int nmult = pl.depthwise ? (pl.dwtc ? pl.Kpad : d->C) : pl.Kpad;
   // padding columns (k >= K) get M = 0 with a fast-path shift so they never force the generic epilogue
   std::vector<int32_t> mult(nmult, 0), rsh(nmult, 33);
   if (pl.requant) {
@@ -433,6 +460,19 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
     else
       e = cudaMemsetAsync(pk + pl.pk_bias, 0, (size_t)d->C * 4, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
+    if (pl.dwtc) {
+      e = launch_pack_dwtc(kernel, d->C, d->R * d->S, pk + pl.pk_dwtc_w, s);
+      if (e != cudaSuccess) return QNN_ERR_CUDA;
+      // per border class: bias - zp_A * sum of the valid taps (depthwise weights = C x R x S x 1)
+      e = launch_fold_offsets(kernel, w_signed, bias, d->C, d->R, d->S, 1, d->input_zero_point, 0, pl.ct,
+                              reinterpret_cast<int32_t*>(pk + pl.pk_off), reinterpret_cast<int64_t*>(pk + pl.pk_off64),
+                              pl.Kpad, s);
+      if (e != cudaSuccess) return QNN_ERR_CUDA;
+      e = cudaMemcpyAsync(pk + pl.pk_rowcls, pl.rowcls.data(), pl.rowcls.size(), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(pk + pl.pk_colcls, pl.colcls.data(), pl.colcls.size(), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return QNN_ERR_CUDA;
+    }
   } else {
     // folded: each filter row r is one GEMM tap whose S*C channels are contiguous in OHWI
     if (pl.fold)
@@ -469,6 +509,12 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   const int a_signed = d->input_dtype == QNN_S8;
 
   if (pl.depthwise) {
+    // kernel choice: 3x3 dp4a (CUDA cores) > tensor-core path > generic CUDA-core kernel.
+    // QNN_DW_IMPL=tc|generic forces one of the others (A/B measurements).
+    static const char* dw_impl = std::getenv("QNN_DW_IMPL");
+    const bool force_tc = dw_impl && std::strcmp(dw_impl, "tc") == 0;
+    const bool force_generic = dw_impl && std::strcmp(dw_impl, "generic") == 0;
+    const bool no_dwtc = force_generic;
     DwParams p{};
     p.in = input;
     p.w = reinterpret_cast<const int16_t*>(pk + pl.pk_w);
@@ -486,6 +532,57 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.requant = pl.requant;
     p.mode = pl.mode;
     p.zp_out = pl.zp_out; p.lo = pl.lo; p.hi = pl.hi;
+    {
+      int64_t wlo, whi;
+      dtype_range(d->kernel_dtype, &wlo, &whi);
+      p.w_fits_s8 = wlo - d->kernel_zero_point >= -128 && whi - d->kernel_zero_point <= 127;
+    }
+    if (!force_tc && !force_generic && pl.requant) {
+      int64_t qlo, qhi;
+      dtype_range(pl.out_dt == DT_S8 ? QNN_S8 : (pl.out_dt == DT_U8 ? QNN_U8 : QNN_S32), &qlo, &qhi);
+      const int clamp = pl.lo > qlo ? 2 : (pl.hi < qhi ? 1 : 0);   // the saturating pack covers the dtype range
+      if (launch_depthwise3(p, clamp, s)) return cuda_status(cudaGetLastError());
+    }
+    if (pl.dwtc && !no_dwtc && pl.requant && (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) &&
+        ((reinterpret_cast<uintptr_t>(input) | reinterpret_cast<uintptr_t>(output)) & 15) == 0) {
+      DwTcParams t{};
+      t.wpk = pk + pl.pk_dwtc_w;
+      t.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
+      t.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
+      t.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
+      t.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
+      t.rowcls = pk + pl.pk_rowcls;
+      t.colcls = pk + pl.pk_colcls;
+      t.out = reinterpret_cast<uint8_t*>(output);
+      t.out_cs = pl.out_cs;
+      t.N = d->N; t.C = d->C; t.Cpad = pl.Kpad; t.P = pl.P; t.Q = pl.Q; t.R = d->R; t.S = d->S;
+      t.sh = d->stride_h; t.sw = d->stride_w; t.pt = d->pad_t; t.pl = d->pad_l;
+      t.ncls = pl.ct.ncr * pl.ct.ncc; t.ncc = pl.ct.ncc;
+      t.idesc = make_idesc_i8(a_signed, 1, 128, 32);
+      t.zp_out = pl.zp_out; t.lo = pl.lo; t.hi = pl.hi;
+      static const char* tr_env = std::getenv("QNN_DWTC_TRACE");
+      t.trace = tr_env ? reinterpret_cast<unsigned long long*>(std::strtoull(tr_env, nullptr, 0)) : nullptr;
+      if (dwtc_plan(t) && load_driver_entry_points()) {
+        // input as a 4-D tensor (c, w, h, n); box = one 32-channel slice x Wp x in_rows pixels with
+        // element strides (sw, sh) for the phase planes; 32-B swizzle = the UMMA SW32 K-major layout
+        alignas(64) CUtensorMap tm;
+        const cuuint64_t dims[4] = {(cuuint64_t)d->C, (cuuint64_t)d->W, (cuuint64_t)d->H, (cuuint64_t)d->N};
+        const cuuint64_t strides[3] = {(cuuint64_t)pl.in_cs, (cuuint64_t)pl.in_cs * d->W,
+                                       (cuuint64_t)pl.in_cs * d->W * d->H};
+        const cuuint32_t box[4] = {32, (cuuint32_t)(t.Wp * t.sw), (cuuint32_t)(t.in_rows * t.sh), 1};
+        const cuuint32_t estr[4] = {1, (cuuint32_t)t.sw, (cuuint32_t)t.sh, 1};
+        CUresult r = p_encode_tiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(input), dims, strides, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        small_tensor_fixup(&tm, (uint64_t)pl.in_cs * d->W * d->H * d->N);
+        if (r == CUDA_SUCCESS) {
+          int64_t qlo, qhi;
+          dtype_range(pl.out_dt == DT_S8 ? QNN_S8 : QNN_U8, &qlo, &qhi);
+          const bool clamp = pl.lo > qlo || pl.hi < qhi;
+          return cuda_status(launch_depthwise_tc(tm, t, pl.mode, clamp, pl.out_dt == DT_S8, s));
+        }
+      }
+    }
     return cuda_status(launch_depthwise(p, s));
   }
 

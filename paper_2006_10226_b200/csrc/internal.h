@@ -122,8 +122,34 @@ struct DwParams {
   int32_t zpA;
   int out_dtype, requant, mode;
   int32_t zp_out, lo, hi;
+  int w_fits_s8;           // every W - zp_W in [-128, 127] (dp4a path)
+  int qseg;                // dp4a path: column blocks per task (set by the launcher)
 };
 cudaError_t launch_depthwise(const DwParams& p, cudaStream_t s);
+bool launch_depthwise3(const DwParams& p, int clamp, cudaStream_t s);   // clamp: 0 none, 1 hi, 2 lo+hi
+
+// Tensor-core depthwise conv (depthwise_tc.cu): C % 16 == 0, s8 weights with zp_W == 0,
+// stride 1 or 2, 8-bit requantized output.
+struct DwTcParams {
+  const uint8_t* wpk;       // [ceil(C/32)][R*S][1024] diagonal B tiles
+  const int32_t* mult;      // [Cpad]
+  const int32_t* rsh;       // [Cpad]
+  const int32_t* off;       // [ncls][Cpad] bias - zp_A * sum_{valid taps} W (int32 wrap)
+  const int64_t* off64;     // [ncls][Cpad] the same, exact
+  const uint8_t* rowcls;    // [P] border row class
+  const uint8_t* colcls;    // [Q] border column class
+  uint8_t* out;             // NHWC, out_cs bytes per pixel
+  long long out_cs;
+  int N, C, Cpad, P, Q, R, S, sh, sw, pt, pl, ncls, ncc;
+  int T, Wp, in_rows, nplanes, region_bytes, stage_bytes, tiles_per_item, nstrips, ncs, items, stages;
+  uint32_t idesc;
+  int32_t zp_out, lo, hi;
+  unsigned long long* trace;   // profiling (QNN_DWTC_TRACE, instrumented builds): CTA 0 timestamps
+};
+bool dwtc_plan(DwTcParams& p);
+cudaError_t launch_depthwise_tc(const CUtensorMap& tmA, const DwTcParams& p, int mode, bool clamp, bool s8out,
+                                cudaStream_t s);
+cudaError_t launch_pack_dwtc(const void* W, int C, int RS, void* wpk, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // Elementwise (elementwise.cu)

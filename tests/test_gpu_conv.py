@@ -198,3 +198,55 @@ def test_errors_raise():
     case = gen.conv_case(700, 1, 8, 6, 6, 8, 3, 3, (1, 1), (1, 1, 1, 1), groups=2)
     with pytest.raises(QnnError):
         gpu_conv(case)
+
+
+# tensor-core depthwise path (C % 32 == 0, s8 weights, zp_W == 0, stride 1/2, 8-bit output):
+# several strips and 128-row tiles, wide rows (Wp > 128), 5x5, asymmetric padding, clamps
+DW_TC = [
+    # N, C, H, W, R, stride, pad(t,l,b,r), a_dtype, out_dtype, act6, mode
+    (2, 32, 30, 37, 3, 1, (1, 1, 1, 1), "u8", "u8", True, "upward"),
+    (1, 64, 7, 7, 3, 1, (1, 1, 1, 1), "u8", "u8", True, "upward"),
+    (3, 96, 14, 14, 3, 2, (1, 1, 1, 1), "u8", "u8", True, "upward"),
+    (1, 32, 57, 150, 3, 1, (1, 1, 1, 1), "u8", "u8", False, "upward"),
+    (2, 64, 19, 23, 5, 1, (2, 2, 2, 2), "s8", "s8", False, "upward"),
+    (2, 32, 20, 21, 5, 2, (2, 2, 2, 2), "u8", "u8", True, "tonearest"),
+    (1, 160, 15, 16, 3, 2, (0, 0, 1, 1), "u8", "s8", False, "tonearest"),
+    (4, 32, 9, 9, 3, 1, (0, 0, 0, 0), "u8", "u8", True, "upward"),
+]
+
+
+@pytest.mark.parametrize("cfg", DW_TC, ids=lambda c: f"C{c[1]}_{c[2]}x{c[3]}_r{c[4]}_s{c[5]}_{c[10]}")
+def test_depthwise_tensor_core_path(cfg):
+    N, C, H, W, R, st, pad, adt, odt, act6, mode = cfg
+    case = gen.conv_case(800 + C + H, N, C, H, W, C, R, R, (st, st), pad, (1, 1), C, adt, "s8", out_dtype=odt,
+                         relu=True, act6=act6, rounding=mode, zp_out=0 if odt == "u8" else -5)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def test_depthwise_forced_kernels_subprocess():
+    """The 3x3 shapes normally take the dp4a kernel; run the tensor-core and the generic
+    kernels on them too (QNN_DW_IMPL is read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+for cfg in [(2, 32, 30, 37, 1, "upward"), (3, 96, 14, 14, 2, "tonearest"), (1, 48, 11, 13, 1, "upward")]:
+    N, C, H, W, st, mode = cfg
+    case = gen.conv_case(900 + C, N, C, H, W, C, 3, 3, (st, st), (1, 1, 1, 1), (1, 1), C, "u8", "s8",
+                         relu=True, act6=True, rounding=mode)
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case)), cfg
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for impl in ("tc", "generic"):
+        env = dict(os.environ, QNN_DW_IMPL=impl)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0 and "OK" in r.stdout, (impl, r.stdout[-2000:], r.stderr[-2000:])
