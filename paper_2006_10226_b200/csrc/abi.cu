@@ -176,6 +176,8 @@ struct ConvPlan {
   // tensor-core path
   bool pad_copy = false;
   bool fold = false;     // width fold: (s, c) -> channels of a copy, filter becomes R x 1 (small-C stems)
+  bool a_build = false;  // fold done in shared memory by the GEMM's builder warps (no X' copy in HBM)
+  int a_ib = 0, a_nr = 0, a_slot_bytes = 0, a_raw_bytes = 0;
   int Ct = 0;            // channel count / pitch seen by TMA
   // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
   int gW = 0, gS = 0, g_sw = 0, g_pl = 0, g_pr = 0, g_dw = 0;
@@ -411,8 +413,39 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   off = align256(off + (size_t)pl.Q);
   pl.pk_total = off;
 
+  // fold with one 32-byte k-block per filter row, resident weights and contiguous rows: the GEMM
+  // kernel builds the X' tiles in shared memory from TMA-staged raw input rows instead of
+  // materialising X' in HBM (QNN_NO_ABUILD=1 keeps the HBM copy, for A/B measurements)
+  static const bool no_abuild = std::getenv("QNN_NO_ABUILD") != nullptr;
+  {
+    const long long rowlen = (long long)d->W * d->C;
+    pl.a_build = !no_abuild && pl.fold && pl.BK == 32 && pl.nchunks == 1 && pl.b_res_kb > 0 &&
+                 d->S * d->C <= 32 && pl.in_cs == d->C && d->dil_w == 1 && rowlen % 16 == 0 &&
+                 (long long)(d->R - 1) * d->dil_h + 1 <= 256;
+    if (pl.a_build) {
+      pl.a_ib = 0;
+      for (int ib : {256, 128, 64, 32, 16})
+        if (rowlen % ib == 0 && rowlen / ib <= 256) {
+          pl.a_ib = ib;
+          break;
+        }
+      pl.a_nr = 127 / pl.Q + 2;
+      pl.a_slot_bytes = (int)((d->R * rowlen + 127) / 128 * 128);
+      pl.a_raw_bytes = (pl.a_nr * pl.a_slot_bytes + 1023) / 1024 * 1024;   // keeps later regions 1 KB aligned
+      const int ncls = pl.ct.ncr * pl.ct.ncc;
+      const int num_kb = d->R;   // one k-block per filter row
+      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, num_kb, pl.a_raw_bytes);
+      if (pl.a_ib == 0 || st < 2 ||
+          gemm_smem_bytes(pl.BK, pl.BN, st, ncls, pl.b_res_kb, num_kb, pl.a_raw_bytes) > 227 * 1024) {
+        pl.a_build = false;
+      } else {
+        pl.kps = num_kb;
+        pl.stages = st;
+      }
+    }
+  }
   size_t w = 0;
-  if (pl.pad_copy || pl.fold) {
+  if (pl.pad_copy || (pl.fold && !pl.a_build)) {
     pl.ws_pad = w;
     w = align256(w + (size_t)d->N * d->H * pl.gW * pl.Ct);
   }
@@ -591,7 +624,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   cudaError_t e;
   const void* A = input;
   long long a_pitch = pl.in_cs;
-  if (pl.fold) {
+  if (pl.fold && !pl.a_build) {
     e = launch_fold_width(input, pl.in_cs, wsb + pl.ws_pad, d->N, d->H, d->W, d->C, pl.Q, d->S, d->stride_w, d->pad_l,
                           d->dil_w, pl.Ct, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
@@ -623,7 +656,19 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   bool ok;
   const int a_chan = (pl.pad_copy || pl.fold) ? pl.Ct : d->C;
   const int taps = d->R * pl.gS;
-  if (pl.im2col)
+  if (pl.a_build) {
+    // raw input rows as (ib bytes, W*C/ib, H, N): one box = R filter rows of one output row
+    const uint64_t rowlen = (uint64_t)d->W * d->C;
+    const cuuint64_t dims[4] = {(cuuint64_t)pl.a_ib, rowlen / pl.a_ib, (cuuint64_t)d->H, (cuuint64_t)d->N};
+    const cuuint64_t strides[3] = {(cuuint64_t)pl.a_ib, rowlen, rowlen * d->H};
+    const cuuint32_t box[4] = {(cuuint32_t)pl.a_ib, (cuuint32_t)(rowlen / pl.a_ib),
+                               (cuuint32_t)((d->R - 1) * d->dil_h + 1), 1};
+    const cuuint32_t estr[4] = {1, 1, (cuuint32_t)d->dil_h, 1};
+    ok = p_encode_tiled(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(input), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    small_tensor_fixup(&tmA, rowlen * d->H * d->N);
+  } else if (pl.im2col)
     ok = encode_im2col(&tmA, A, a_chan, pl.gW, d->H, d->N, (uint64_t)a_pitch, -pl.g_pl, -d->pad_t,
                        pl.g_pr - (pl.gS - 1) * pl.g_dw, d->pad_b - (d->R - 1) * d->dil_h, pl.BK, pl.g_sw,
                        d->stride_h);
@@ -643,7 +688,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
                          (reinterpret_cast<uintptr_t>(output) & 15) == 0;
   if (tma_store) {
     // column groups of one epilogue warp set (gemm_epi_sets): 4 / nsets
-    const int nchunk = pl.BN / 32, ng = 4 / gemm_epi_sets(pl.BN, pl.num_n);
+    const int nepi = pl.a_build ? 8 : kGemmEpiWarps;
+    const int nchunk = pl.BN / 32, ng = (nepi / 4) / gemm_epi_sets(pl.BN, pl.num_n, nepi);
     for (int h = 0; h < ng; ++h) {
       const int width = ((h + 1) * nchunk / ng - h * nchunk / ng) * 32;
       const int wb = width ? width : 32;
@@ -682,6 +728,16 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.trace = tr_env ? reinterpret_cast<unsigned long long*>(std::strtoull(tr_env, nullptr, 0)) : nullptr;
   }
   p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = pl.g_sw; p.pt = d->pad_t; p.pl = pl.g_pl;
+  p.fdQ = make_fastdiv((uint32_t)pl.Q);
+  p.fdPQ = make_fastdiv((uint32_t)(pl.P * pl.Q));
+  if (pl.a_build) {
+    p.a_build = 1;
+    p.a_W = d->W; p.a_C = d->C; p.a_S = d->S; p.a_sw = d->stride_w; p.a_pl = d->pad_l;
+    p.a_rowlen = d->W * d->C;
+    p.a_nr = pl.a_nr;
+    p.a_slot_bytes = pl.a_slot_bytes;
+    p.a_raw_bytes = pl.a_raw_bytes;
+  }
   p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8, kGemmBM, pl.BN);
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);

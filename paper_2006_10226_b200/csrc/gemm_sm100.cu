@@ -49,17 +49,26 @@ constexpr bool kInstrument = false;
 // the pipeline stages carry A only.
 // Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
 // commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps) {
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes) {
   const size_t a = (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
   const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * b : stages * (a + b * kps);
-  return 1024 + ring + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
+  return 1024 + ring + (size_t)stages * raw_bytes + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
 }
 
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps) {
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes) {
   const size_t budget = 227 * 1024;
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps) > budget) --s;
+  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes) > budget) --s;
   return s;
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
 }
 
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
@@ -78,13 +87,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int BK = p.BK, BN = p.BN, stages = p.stages;
   const int nacc = gemm_acc_bufs(BN), acc_log = nacc == 8 ? 3 : (nacc == 4 ? 2 : 1);
   const uint32_t acc_cols = 512u / nacc;
-  const int nsets = gemm_epi_sets(BN, p.num_n_tiles);
+  // a_build: warps 8..15 build A tiles, warps 0..7 run the epilogue
+  const int nepi = p.a_build ? 8 : kGemmEpiWarps;
+  const int nsets = gemm_epi_sets(BN, p.num_n_tiles, nepi);
   const uint32_t a_bytes = kGemmBM * BK, b_bytes = BN * BK;
   const bool b_res = p.b_res;
   const int kps = p.kps;                   // k-blocks per pipeline stage
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * kps * a_bytes;   // ring of B stages, or the resident B (num_kb blocks)
-  uint8_t* sOut = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);
+  uint8_t* sRaw = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);   // a_build rows
+  uint8_t* sOut = sRaw + (size_t)stages * p.a_raw_bytes;
   const bool tracing = kInstrument && p.trace != nullptr && blockIdx.x == 0;
   const int dbg = kInstrument ? p.dbg : 0;
   int2* sMT = reinterpret_cast<int2*>(sOut + kStageOutBytes);          // {M, t} per column
@@ -97,7 +109,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 8;
   uint64_t* bres_full = tempty + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* rawfull = bres_full + 1;   // a_build: raw input rows of a stage landed (TMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawfull + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-critical
@@ -116,14 +129,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tma_prefetch_desc(&tmC3);
     }
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], p.a_build ? kEpiW - nepi : 1);   // a_build: one arrive per builder warp
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < nacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kGemmEpiWarps / nsets);   // every warp of the set that owns the tile
+      mbar_init(&tempty[a], nepi / nsets);   // every warp of the set that owns the tile
     }
     mbar_init(bres_full, 1);
+    for (int s = 0; s < stages; ++s) mbar_init(&rawfull[s], 1);
     fence_mbar_init();
   }
   if (tracing && threadIdx.x == 0) trace_at(p.trace, 6000);
@@ -166,7 +180,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     const bool skip_a = dbg & 4;
     int m_blk = m_first, n_blk = n_first;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    if (p.a_build) {
+      // raw input rows for the builders: per output row the tile touches, its R filter rows
+      // (zero outside the image: TMA OOB fill), one 4-D box each
+      const uint32_t bytes = (uint32_t)p.a_nr * p.num_kb * p.a_rowlen;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int r_first = (m_blk * kGemmBM) / p.Q;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) {
+          mbar_arrive_expect_tx(&rawfull[stage], bytes);
+          uint8_t* dst = sRaw + (size_t)stage * p.a_raw_bytes;
+          for (int k = 0; k < p.a_nr; ++k) {
+            const int ri = r_first + k, n = ri / p.P, pp = ri - n * p.P;
+            tma_load_4d(dst + (size_t)k * p.a_slot_bytes, &tmA, &rawfull[stage], 0, 0, pp * p.sh - p.pt, n);
+          }
+        }
+        __syncwarp();
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        QNN_NEXT_TILE();
+      }
+    }
+    for (int t = p.a_build ? num_tiles : blockIdx.x; t < num_tiles; t += gridDim.x) {   // a_build: done above
       const int m0 = m_blk * kGemmBM;
       int an = 0, ah = 0, aw = 0;
       if (p.im2col) {
@@ -217,6 +254,70 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       QNN_NEXT_TILE();
     }
+  } else if (p.a_build && warp >= nepi && warp < kEpiW) {
+    // ------------------------------------------------------------ A-tile builders
+    // Item (pixel mi, filter row r) of a tile: row mi of k-block r = X'[n, p*sh + r*dil_h - pt,
+    // q, 0..32) for output pixel m0 + mi = (n, p, q): the S*C bytes of raw row (p, r) from
+    // column q*sw - pl on (zero outside the row), in the 32-B swizzle of the UMMA descriptor.
+    // Bytes past S*C are left as they come: the packed weights are zero there.  The raw rows
+    // are in shared memory (TMA, see the producer): [output-row slot][r][W*C bytes].
+    // 8 builder warps = 256 threads: thread bt owns pixel bt % 128 and the filter rows
+    // r = bt / 128, +2, +4, ... (pixel decode once per tile)
+    const int bt = (warp - nepi) * 32 + lane;
+    const int mi = bt & (kGemmBM - 1), r0 = bt >> 7;
+    const int SC = p.a_S * p.a_C;
+    const int rowlen = p.a_rowlen;
+    const uint32_t swz = ((uint32_t)mi >> 2) & 1u;   // 32-B swizzle of this row
+    int stage = 0;
+    uint32_t phase = 0;
+    int m_blk = m_first, n_blk = n_first;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = m_blk * kGemmBM;
+      const int r_first = (int)fdiv((uint32_t)m0, p.fdQ);
+      const int row = m0 + mi;
+      const int ri = (int)fdiv((uint32_t)row, p.fdQ), qq = row - ri * p.Q;
+      const int o = (qq * p.a_sw - p.a_pl) * p.a_C;   // window start in the row (may be < 0)
+      const int ab = o & ~3;
+      const uint32_t sh8 = (uint32_t)(o - ab) * 8u;
+      const bool border = o < 0 || o + SC > rowlen;
+      const int jlo = max(0, -o), jhi = min(SC, rowlen - o);
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_wait(&rawfull[stage], phase);
+      const uint8_t* rp0 = sRaw + (size_t)stage * p.a_raw_bytes + (size_t)(ri - r_first) * p.a_slot_bytes + ab;
+      uint8_t* dA = sA + (size_t)(stage * kps) * a_bytes + (size_t)mi * 32;
+      for (int r = r0; r < p.num_kb; r += 2) {
+        // 9 aligned words around the window (addresses outside the row only feed masked bytes
+        // and stay inside this CTA's shared memory); bytes past S*C are left as they come:
+        // the packed weights are zero there
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(rp0 + (size_t)r * rowlen);
+        uint32_t u[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) u[k] = wp[k];
+        uint32_t wv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wv[k] = __funnelshift_r(u[k], u[k + 1], sh8);
+        if (border) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int l = min(max(jlo - 4 * k, 0), 4), h = min(max(jhi - 4 * k, 0), 4);
+            const uint32_t mh = h == 4 ? 0xFFFFFFFFu : ((1u << (8 * h)) - 1u);
+            const uint32_t ml = l == 4 ? 0xFFFFFFFFu : ((1u << (8 * l)) - 1u);
+            wv[k] &= h > l ? (mh & ~ml) : 0u;
+          }
+        }
+        uint8_t* rowdst = dA + (size_t)r * a_bytes;
+        *reinterpret_cast<uint4*>(rowdst + (swz << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4*>(rowdst + ((swz ^ 1u) << 4)) = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[stage]);
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+      QNN_NEXT_TILE();
+    }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; the elected lane issues every tcgen05.mma and its commits.
@@ -263,7 +364,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (tracing && leader && it < 100) trace_at(p.trace, 7400 + it);
       __syncwarp();
     }
-  } else if (warp < kEpiW) {
+  } else if (warp < nepi) {
     // ------------------------------------------------------------ epilogue
     // 16 warps in nsets sets taking alternate tiles; within a set, warp w reads TMEM lanes
     // [32*(w%4), +32) (its quad of rows) and the contiguous chunk range of its column
@@ -272,7 +373,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int et = threadIdx.x;
     const int ew = warp;
     const int quad = warp & 3;
-    const int wps = kGemmEpiWarps / nsets;        // warps per set
+    const int wps = nepi / nsets;                 // warps per set
     const int set = ew / wps;
     const int ngrp = wps >> 2;                    // column groups per set
     const int grp = (ew - set * wps) >> 2;
@@ -288,7 +389,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int row_bytes = (c_end - c_begin) * 32;
     const uint32_t swz_mask = row_bytes == 128 ? 7u : (row_bytes == 64 ? 3u : (row_bytes == 32 ? 1u : 0u));
     const CUtensorMap* tmC = grp == 0 ? &tmC0 : (grp == 1 ? &tmC1 : (grp == 2 ? &tmC2 : &tmC3));
-    constexpr int kEpiThreads = 32 * kGemmEpiWarps;
+    const int kEpiThreads = 32 * nepi;
     int cur_n = -1, tile_fast = 1;
     const bool has_rt = e.rowsum != nullptr;
     int m_blk = m_first, n_blk = n_first;
@@ -358,8 +459,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int32_t rterm = 0;
       if (row_ok) {
         if (HAS_CLS) {
-          const int rem = row % pq;
-          const int pp = rem / p.Q, qq = rem - pp * p.Q;
+          const int rem = row - (int)fdiv((uint32_t)row, p.fdPQ) * pq;
+          const int pp = (int)fdiv((uint32_t)rem, p.fdQ), qq = rem - pp * p.Q;
           cls = (int)e.rowcls[pp] * e.ncc + (int)e.colcls[qq];
         }
         if (e.rowsum) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
@@ -532,7 +633,8 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
     if (e != cudaSuccess) return e;
     if (dev < 64) attr_done[dev] = 1;
   }
-  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb : 0, p.kps);
+  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb : 0, p.kps,
+                                      p.a_raw_bytes);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();

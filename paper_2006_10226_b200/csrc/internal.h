@@ -36,6 +36,28 @@ struct GemmEpilogue {
   int32_t zp_out, lo, hi;  // lo/hi already include ReLU, act clamp and dtype range
 };
 
+// Division by a runtime divisor d >= 1 for dividends in [0, 2^31): q = umulhi(x, mul) >> shr
+// with p = 31 + ceil(log2 d), mul = ceil(2^p / d), shr = p - 32 (d == 1: mul = 0, identity).
+struct FastDiv {
+  uint32_t d, mul, shr;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d > 1) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    const uint32_t p = 31 + l;
+    f.mul = (uint32_t)(((1ull << p) + d - 1) / d);
+    f.shr = p - 32;
+  }
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+  return f.d == 1 ? x : (__umulhi(x, f.mul) >> f.shr);
+}
+#endif
+
 struct GemmParams {
   int M, Nout;
   int num_kb, nchunks, S, dil_h, dil_w;
@@ -51,7 +73,17 @@ struct GemmParams {
                            // 4 no A loads, 8 no MMAs, 16 no TMEM loads; results are then garbage
   unsigned long long* trace; // profiling: CTA 0 event timestamps (QNN_GEMM_TRACE), else nullptr
   int P, Q, sh, sw, pt, pl;
+  FastDiv fdQ, fdPQ;       // output-row decode: /Q and /(P*Q)
   uint32_t idesc;
+  // a_build: the A tiles of a width-folded conv (X'[n, h, q, s*C + c] = A[n, h, q*sw + s*dw - pl, c])
+  // are built in shared memory by two builder warps straight from the raw NHWC input, instead of
+  // materialising X' in HBM and reading it back with TMA (same bytes, same border classes)
+  int a_build;
+  int a_W, a_C, a_S, a_sw, a_pl;
+  int a_rowlen;            // bytes of one input row (W * C, contiguous channels)
+  int a_nr;                // output rows a 128-pixel tile can touch: raw rows staged per tile = a_nr * R
+  int a_slot_bytes;        // one output row's R raw rows (R * a_rowlen rounded up to 128 B: TMA alignment)
+  int a_raw_bytes;         // per-stage raw-row region (a_nr * a_slot_bytes)
   GemmEpilogue e;
 };
 
@@ -67,17 +99,19 @@ __host__ __device__ inline int gemm_acc_bufs(int BN) {
   return n;
 }
 // Epilogue warp sets: with fewer than four 32-column chunks per tile and a single N
-// tile, the 16 epilogue warps split into sets that take alternate tiles (each set
-// still covers all 128 rows: 4 quads x 4/nsets column groups).
-__host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles) {
+// tile, the nepi epilogue warps split into sets that take alternate tiles (each set
+// still covers all 128 rows: 4 quads x (nepi/4)/nsets column groups).  nepi is 16, or 8
+// when half of them build A tiles (a_build).
+__host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles, int nepi = kGemmEpiWarps) {
   const int nchunk = BN / 32;
   if (num_n_tiles != 1 || nchunk >= 3) return 1;
-  return 4 / nchunk;   // 1 chunk -> 4 sets, 2 chunks -> 2 sets
+  const int s = 4 / nchunk;   // 1 chunk -> 4 sets, 2 chunks -> 2 sets
+  return s < nepi / 4 ? s : nepi / 4;
 }
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps);
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps);
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0);
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 

@@ -250,3 +250,56 @@ print("OK")
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                            timeout=600)
         assert r.returncode == 0 and "OK" in r.stdout, (impl, r.stdout[-2000:], r.stderr[-2000:])
+
+
+# width-folded small-C convolutions (stems): the GEMM builds X' tiles in shared memory
+FOLD_CASES = [
+    # N, C, H, W, K, R, S, stride, pad(t,l,b,r), dil, a_dtype, w_dtype, zp_W
+    (2, 3, 33, 35, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0),
+    (1, 4, 17, 19, 32, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "s8", "s8", 0),
+    (2, 8, 15, 13, 48, 3, 3, (2, 2), (1, 0, 1, 2), (1, 1), "u8", "s8", 0),
+    (1, 3, 20, 21, 16, 5, 5, (1, 1), (2, 2, 2, 2), (1, 2), "u8", "s8", 0),
+    (1, 6, 12, 12, 40, 5, 5, (1, 1), (2, 2, 2, 2), (1, 1), "u8", "s8", 0),
+    (3, 3, 9, 9, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0),
+    (2, 3, 23, 24, 32, 3, 3, (2, 2), (1, 1, 1, 1), (1, 1), "u8", "u8", 119),
+    # W*C % 16 == 0: X' tiles built in shared memory from TMA-staged raw rows
+    (2, 3, 37, 32, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0),
+    (1, 4, 20, 24, 32, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "s8", "s8", 0),
+    (2, 8, 15, 14, 48, 3, 3, (2, 2), (1, 0, 1, 2), (1, 1), "u8", "s8", 0),
+    (1, 6, 16, 16, 40, 5, 5, (1, 1), (2, 2, 2, 2), (1, 1), "u8", "s8", 0),
+    (3, 3, 16, 16, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0),
+    (2, 3, 32, 32, 32, 3, 3, (2, 2), (1, 1, 1, 1), (1, 1), "u8", "u8", 119),
+    (1, 4, 20, 20, 16, 3, 3, (1, 1), (2, 1, 2, 1), (2, 1), "u8", "s8", 0),
+    (1, 3, 64, 224, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), "u8", "s8", 0),
+]
+
+
+@pytest.mark.parametrize("cfg", FOLD_CASES, ids=lambda c: f"C{c[1]}_{c[2]}x{c[3]}_k{c[5]}x{c[6]}_s{c[7][0]}")
+def test_folded_small_channel_conv(cfg):
+    N, C, H, W, K, R, S, st, pad, dil, adt, wdt, zpW = cfg
+    case = gen.conv_case(1100 + C * 7 + H, N, C, H, W, K, R, S, st, pad, dil, 1, adt, wdt, zp_W=zpW,
+                         per_channel=zpW == 0)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def test_folded_conv_hbm_copy_path_subprocess():
+    """QNN_NO_ABUILD=1 takes the materialised-X' path (fold kernel + TMA im2col) instead."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+case = gen.conv_case(1200, 2, 3, 33, 35, 64, 7, 7, (2, 2), (3, 3, 3, 3), (1, 1), 1, "u8", "s8")
+_, _, y = gpu_conv(case)
+assert np.array_equal(y.cpu().numpy(), oracle_conv(case))
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_ABUILD="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
