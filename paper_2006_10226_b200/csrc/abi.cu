@@ -178,6 +178,7 @@ struct ConvPlan {
   bool fold = false;     // width fold: (s, c) -> channels of a copy, filter becomes R x 1 (small-C stems)
   bool a_build = false;  // fold done in shared memory by the GEMM's builder warps (no X' copy in HBM)
   int a_ib = 0, a_nr = 0, a_slot_bytes = 0, a_raw_bytes = 0;
+  bool a_zpfill = false;  // a_build writes zp_A outside the image (single border class)
   int Ct = 0;            // channel count / pitch seen by TMA
   // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
   int gW = 0, gS = 0, g_sw = 0, g_pl = 0, g_pr = 0, g_dw = 0;
@@ -395,24 +396,6 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, ncls, pl.b_res_kb, pl.kps) > 227 * 1024) return QNN_ERR_UNSUPPORTED;
   }
 
-  const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
-  size_t off = 0;
-  pl.pk_w = off;
-  off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
-  pl.pk_off = off;
-  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
-  pl.pk_off64 = off;
-  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 8);
-  pl.pk_mult = off;
-  off = align256(off + (size_t)pl.Kpad * 4);
-  pl.pk_rsh = off;
-  off = align256(off + (size_t)pl.Kpad * 4);
-  pl.pk_rowcls = off;
-  off = align256(off + (size_t)pl.P);
-  pl.pk_colcls = off;
-  off = align256(off + (size_t)pl.Q);
-  pl.pk_total = off;
-
   // fold with one 32-byte k-block per filter row, resident weights and contiguous rows: the GEMM
   // kernel builds the X' tiles in shared memory from TMA-staged raw input rows instead of
   // materialising X' in HBM (QNN_NO_ABUILD=1 keeps the HBM copy, for A/B measurements)
@@ -443,7 +426,36 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
         pl.stages = st;
       }
     }
+    if (pl.a_build && d->kernel_zero_point == 0) {
+      // the builders write zp_A (not 0) outside the image, so every tap is valid: one border
+      // class, off = bias - zp_A * sum_taps W, and a per-class-free epilogue (zp_W == 0: no row sums)
+      pl.a_zpfill = true;
+      pl.ct.ncr = pl.ct.ncc = 1;
+      pl.ct.r_lo[0] = 0; pl.ct.r_hi[0] = d->R - 1;
+      pl.ct.s_lo[0] = 0; pl.ct.s_hi[0] = d->S - 1;
+      pl.rowcls.assign(pl.P, 0);
+      pl.colcls.assign(pl.Q, 0);
+      pl.stages = gemm_max_stages(pl.BK, pl.BN, 1, pl.b_res_kb, pl.kps, pl.a_raw_bytes);
+    }
   }
+  const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
+  size_t off = 0;
+  pl.pk_w = off;
+  off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
+  pl.pk_off = off;
+  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
+  pl.pk_off64 = off;
+  off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 8);
+  pl.pk_mult = off;
+  off = align256(off + (size_t)pl.Kpad * 4);
+  pl.pk_rsh = off;
+  off = align256(off + (size_t)pl.Kpad * 4);
+  pl.pk_rowcls = off;
+  off = align256(off + (size_t)pl.P);
+  pl.pk_colcls = off;
+  off = align256(off + (size_t)pl.Q);
+  pl.pk_total = off;
+
   size_t w = 0;
   if (pl.pad_copy || (pl.fold && !pl.a_build)) {
     pl.ws_pad = w;
@@ -735,6 +747,10 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.a_W = d->W; p.a_C = d->C; p.a_S = d->S; p.a_sw = d->stride_w; p.a_pl = d->pad_l;
     p.a_rowlen = d->W * d->C;
     p.a_nr = pl.a_nr;
+    p.a_H = d->H;
+    p.a_zpfill = pl.a_zpfill;
+    p.a_zp4 = 0x01010101u * (uint32_t)(d->input_zero_point & 0xFF);
+    p.fdP = make_fastdiv((uint32_t)pl.P);
     p.a_slot_bytes = pl.a_slot_bytes;
     p.a_raw_bytes = pl.a_raw_bytes;
   }

@@ -281,6 +281,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t sh8 = (uint32_t)(o - ab) * 8u;
       const bool border = o < 0 || o + SC > rowlen;
       const int jlo = max(0, -o), jhi = min(SC, rowlen - o);
+      // a_zpfill: output row p of this pixel, for the filter rows that fall outside the image
+      const int h0 = p.a_zpfill ? ((ri - (int)fdiv((uint32_t)ri, p.fdP) * p.P) * p.sh - p.pt) : 0;
+      const uint32_t fill = p.a_zpfill ? p.a_zp4 : 0u;
       mbar_wait(&empty[stage], phase ^ 1);
       mbar_wait(&rawfull[stage], phase);
       const uint8_t* rp0 = sRaw + (size_t)stage * p.a_raw_bytes + (size_t)(ri - r_first) * p.a_slot_bytes + ab;
@@ -302,7 +305,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int l = min(max(jlo - 4 * k, 0), 4), h = min(max(jhi - 4 * k, 0), 4);
             const uint32_t mh = h == 4 ? 0xFFFFFFFFu : ((1u << (8 * h)) - 1u);
             const uint32_t ml = l == 4 ? 0xFFFFFFFFu : ((1u << (8 * l)) - 1u);
-            wv[k] &= h > l ? (mh & ~ml) : 0u;
+            const uint32_t m = h > l ? (mh & ~ml) : 0u;
+            wv[k] = (wv[k] & m) | (fill & ~m);
+          }
+        }
+        if (p.a_zpfill) {
+          const int hh = h0 + r * p.dil_h;
+          if (hh < 0 || hh >= p.a_H) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) wv[k] = fill;
           }
         }
         uint8_t* rowdst = dA + (size_t)r * a_bytes;
@@ -485,12 +496,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_ld32_nowait(tbase + c_begin * 32 + 32, vb);
         tmem_wait32(va);
         tmem_wait32(vb);
+        if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
+        if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 1);
         const long long* kbase = reinterpret_cast<const long long*>(sOff) + cls * offp + c_begin * 32;
         const int4* mt4 = reinterpret_cast<const int4*>(sMT + c_begin * 32);
         uint32_t w[8];
@@ -502,6 +515,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           epi_chunk_up<CLAMP, S8OUT, false>(va, mt4, reinterpret_cast<const longlong2*>(kbase), rterm, lo, hi, w);
         *reinterpret_cast<uint4*>(stage_out + (l16 ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(stage_out + ((l16 + 16) ^ sw)) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 2);
         if (has_rt)
           epi_chunk_up<CLAMP, S8OUT, true>(vb, mt4 + 16, reinterpret_cast<const longlong2*>(kbase + 32), rterm, lo,
                                            hi, w);
@@ -510,6 +524,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                             hi, w);
         *reinterpret_cast<uint4*>(stage_out + ((l16 + 32) ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(stage_out + ((l16 + 48) ^ sw)) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 3);
       }
 #pragma unroll 1
       for (int j = two ? c_end : c_begin; j < c_end; ++j) {

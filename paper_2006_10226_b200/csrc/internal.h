@@ -82,6 +82,9 @@ struct GemmParams {
   int a_W, a_C, a_S, a_sw, a_pl;
   int a_rowlen;            // bytes of one input row (W * C, contiguous channels)
   int a_nr;                // output rows a 128-pixel tile can touch: raw rows staged per tile = a_nr * R
+  int a_H, a_zpfill;       // a_zpfill: bytes outside the image are zp_A (single border class)
+  uint32_t a_zp4;          // zp_A replicated into 4 bytes
+  FastDiv fdP;
   int a_slot_bytes;        // one output row's R raw rows (R * a_rowlen rounded up to 128 B: TMA alignment)
   int a_raw_bytes;         // per-stage raw-row region (a_nr * a_slot_bytes)
   GemmEpilogue e;

@@ -2,7 +2,7 @@
 import os, sys, json
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-buf = torch.zeros(16384, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16384, dtype=torch.int64, device="cuda")  # slots < 16384
 os.environ["QNN_GEMM_TRACE"] = str(buf.data_ptr())
 from tools.bench_layers import conv_layer  # noqa
 from workloads.shapes import resnet50_unique
@@ -28,7 +28,14 @@ pw0, pw1, pi = t[6300:6556], t[0:256], t[6600:6856]
 n = int(((pw0 > 0) & (pi > 0)).sum())
 print("producer: wait(empty) cost:", (pw1[:n] - pw0[:n])[:16].tolist())
 print("producer: issue cost      :", (pi[:n] - pw1[:n])[:16].tolist())
-print("producer: loop overhead   :", (pw0[1:n] - pi[:n-1])[:16].tolist())
+if n > 1:
+    print("producer: loop overhead   :", (pw0[1:n] - pi[:n-1])[:16].tolist())
+ep = t[12000:12000 + 8 * 60].reshape(60, 8)
+print("epilogue warp0 'two' path: tmem-loaded, store-buffer-free, chunkA, chunkB  (rel. to tfull wake)")
+for i in range(0, 40, 2):
+    if ep[i, 0] > 0:
+        w = t[5120 + i]
+        print(i, [int(x - w) if x > 0 else None for x in ep[i, :4]])
 mw0, mw1 = t[6900:7156], t[2048:2048+256]
 n2 = int((mw0 > 0).sum())
 print("mma: wait(full) cost:", (mw1[:n2] - mw0[:n2])[:20].tolist())
