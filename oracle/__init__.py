@@ -72,6 +72,11 @@ def lib():
             L.oracle_quantize.argtypes = [vp, i64, i64, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int, vp]
             L.oracle_dequantize.argtypes = [vp, ctypes.c_int, i64, i64, ctypes.c_int, vp, vp, ctypes.c_int, vp]
             L.oracle_num_threads.restype = ctypes.c_int
+            f32 = ctypes.c_float
+            L.oracle_add.argtypes = [vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32, i64, f32, i32,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
+            L.oracle_add.restype = ctypes.c_int
+            L.oracle_pool2d.argtypes = [vp] + [ctypes.c_int] * 14 + [vp]
             _lib = L
     return _lib
 
@@ -289,3 +294,54 @@ def _finish(acc, s_A, s_W, out, axis):
     return requantize_acc(acc, M, S, out.get("dtype", "u8"), out.get("zero_point", 0),
                           out.get("rounding", "upward"), out.get("relu", False),
                           out.get("act_min"), out.get("act_max"), axis=axis)
+
+
+# --------------------------------------------------------------------------- #
+# Inter-layer glue: qnn.add, pooling, conv + residual add   #
+# --------------------------------------------------------------------------- #
+def add(a, s_a, zp_a, b, s_b, zp_b, s_out, zp_out, out_dtype="u8", rounding="upward", relu=False):
+    """qnn.add: clamp(zp_out + R((a - zp_a) s_a/s_out) + R((b - zp_b) s_b/s_out)) (reading R19)."""
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    assert a.shape == b.shape
+    out = np.zeros(a.shape, NP_DT[out_dtype])
+    rc = lib().oracle_add(_p(a), DT[_dt_of(a)], ctypes.c_float(s_a), int(zp_a), _p(b), DT[_dt_of(b)],
+                          ctypes.c_float(s_b), int(zp_b), a.size, ctypes.c_float(s_out), int(zp_out),
+                          ROUND[rounding], int(bool(relu)), DT[out_dtype], _p(out))
+    if rc != 0:
+        raise ValueError("invalid add scales")
+    return out
+
+
+def pool2d(x, mode, R, S, stride=(1, 1), pad=(0, 0, 0, 0)):
+    """Max / average pooling on quantized NCHW values (readings R17, R20)."""
+    x = np.ascontiguousarray(x)
+    N, C, H, W = x.shape
+    P, Q = out_hw(H, W, R, S, stride, pad)
+    out = np.zeros((N, C, P, Q), x.dtype)
+    lib().oracle_pool2d(_p(x), DT[_dt_of(x)], int(mode == "avg"), N, C, H, W, R, S, stride[0], stride[1],
+                        pad[0], pad[1], P, Q, _p(out))
+    return out
+
+
+def qnn_conv2d_add(A, Wt, zp_A, zp_W, s_A, s_W, bias, res, s_res, zp_res, out, stride=(1, 1),
+                   pad=(0, 0, 0, 0), dil=(1, 1), groups=1):
+    """qnn.conv2d whose int32 result, requantized to (s_out, 0), is added to a residual input
+    requantized the same way (qnn.add of the conv's int32 output and the residual, then ReLU /
+    clamps): y = clamp(zp_out + R(acc * m_k) + R((res - zp_res) * s_res / s_out)).  NCHW."""
+    acc = conv2d_acc(A, Wt, zp_A, zp_W, bias, stride, pad, dil, groups)
+    K = Wt.shape[0]
+    M, S = conv_multipliers(s_A, s_W, out["scale"], K)
+    rnd = out.get("rounding", "upward")
+    y = requantize_acc(acc, M, S, "s32", 0, rnd, axis=1).astype(np.int64)
+    y += requantize(np.ascontiguousarray(res), [s_res], zp_res, out["scale"], 0, "s32", rnd).astype(np.int64)
+    y += int(out.get("zero_point", 0))
+    zp_out = int(out.get("zero_point", 0))
+    lo, hi = RANGE[out.get("dtype", "u8")]
+    if out.get("relu", False):
+        lo = max(lo, zp_out)
+    if out.get("act_min") is not None:
+        lo = max(lo, int(out["act_min"]))
+    if out.get("act_max") is not None:
+        hi = min(hi, int(out["act_max"]))
+    return np.clip(y, lo, hi).astype(NP_DT[out.get("dtype", "u8")])

@@ -394,6 +394,76 @@ void oracle_dequantize(const void* q, int in_dt, int64_t count, int64_t inner, i
   }
 }
 
+/* ------------------------------------------------------------------------- *
+ * Inter-layer glue (the paper's framework operators
+ * "quantized_add", pooling).
+ * ------------------------------------------------------------------------- */
+
+/* qnn.add: each input is requantized (Eq. 5 with the fixed-point proxy, R2/R3)
+ * to (s_out, zero point 0) as an exact integer, the two are summed, zp_out is
+ * added, optional ReLU (lower bound zp_out), then saturation to the output
+ * dtype (reading R19; SPEC canonicalize_add).  Returns -1 on a bad scale. */
+int oracle_add(const void* a, int a_dt, float s_a, int32_t zp_a, const void* b, int b_dt, float s_b,
+               int32_t zp_b, int64_t count, float s_out, int32_t zp_out, int mode, int relu, int out_dt,
+               void* out) {
+  int32_t Ma, Sa, Mb, Sb;
+  if (oracle_derive_multiplier((double)s_a / (double)s_out, &Ma, &Sa) != 0) return -1;
+  if (oracle_derive_multiplier((double)s_b / (double)s_out, &Mb, &Sb) != 0) return -1;
+  int64_t lo, hi;
+  dtype_range(out_dt, &lo, &hi);
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t ya = oracle_round_fixed(load_q(a, a_dt, i) - zp_a, Ma, Sa, mode);
+    const int64_t yb = oracle_round_fixed(load_q(b, b_dt, i) - zp_b, Mb, Sb, mode);
+    int64_t y = ya + yb + zp_out;
+    if (relu && y < zp_out) y = zp_out;
+    if (y < lo) y = lo;
+    if (y > hi) y = hi;
+    store_q(out, out_dt, i, y);
+  }
+  return 0;
+}
+
+/* Pooling on the quantized values, input and output sharing (scale, zero
+ * point) as the frontend enforces (SPEC canonicalize_*_pool).  NCHW.
+ * Padding taps are excluded (max: -inf; avg: not counted, reading R20).
+ *   max: Q_out = max over the valid window (max commutes with the monotone
+ *        affine map of Eq. 1).
+ *   avg: s = sum of the valid taps (int64; the paper's int16 upcast cannot hold
+ *        a sum of more than 128 u8 values, R17), n = number of valid taps,
+ *        Q_out = sign(s) * floor((2|s| + n) / (2n))  (rounding division with ties
+ *        away from zero, SPEC "ToNearestAway"). */
+void oracle_pool2d(const void* in, int dt, int is_avg, int N, int C, int H, int W, int R, int S, int sh,
+                   int sw, int pt, int pl, int P, int Q, void* out) {
+  #pragma omp parallel for collapse(2) schedule(static)
+  for (int n = 0; n < N; ++n)
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < Q; ++q) {
+          int64_t best = INT64_MIN, sum = 0, cnt = 0;
+          for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+              const int h = p * sh + r - pt, w = q * sw + s - pl;
+              if (h < 0 || h >= H || w < 0 || w >= W) continue;
+              const int64_t v = load_q(in, dt, (((int64_t)n * C + c) * H + h) * W + w);
+              if (v > best) best = v;
+              sum += v;
+              ++cnt;
+            }
+          int64_t y = 0;
+          if (is_avg) {
+            if (cnt > 0) {
+              const int64_t a = sum < 0 ? -sum : sum;
+              const int64_t m = (2 * a + cnt) / (2 * cnt);
+              y = sum < 0 ? -m : m;
+            }
+          } else {
+            y = cnt > 0 ? best : 0;
+          }
+          store_q(out, dt, (((int64_t)n * C + c) * P + p) * Q + q, y);
+        }
+}
+
 int oracle_num_threads(void);
 }  /* extern "C" */
 
