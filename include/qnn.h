@@ -221,6 +221,41 @@ QNN_API qnn_status_t qnn_dequantize(const void* in, qnn_dtype_t in_dtype, float*
                             int32_t ndim, int32_t axis, const float* scales, const int32_t* zero_points,
                             int32_t n_params, qnn_stream_t stream);
 
+/* -------------------------------------------------------------------------------------------
+ * Inter-layer glue (the paper's framework operators quantized_add and
+ * pooling).
+ * ------------------------------------------------------------------------------------------- */
+
+/* qnn.add (reading R19, SPEC canonicalize_add): each input is requantized (Eq. 5, fixed-point
+ * multiplier of s_x / s_out, `rounding`) to (s_out, zero point 0), the two int32 values are
+ * summed, zp_out is added, then max(., zp_out) if relu, then saturation to out_dtype:
+ *   out[i] = sat(max?(zp_out + R((a[i]-zp_a) s_a/s_out) + R((b[i]-zp_b) s_b/s_out)))
+ * a, b, out: `count` elements each, S8/U8 (device pointers, same element order).  Per-tensor
+ * scales only.  Errors: INVALID_VALUE for a bad scale / zero point / dtype, UNSUPPORTED for a
+ * scale ratio >= 2^30. */
+QNN_API qnn_status_t qnn_add(const void* a, qnn_dtype_t a_dtype, float s_a, int32_t zp_a, const void* b,
+                             qnn_dtype_t b_dtype, float s_b, int32_t zp_b, void* out, qnn_dtype_t out_dtype,
+                             float s_out, int32_t zp_out, int64_t count, qnn_rounding_t rounding, int32_t relu,
+                             qnn_stream_t stream);
+
+typedef enum { QNN_POOL_MAX = 0, QNN_POOL_AVG = 1 } qnn_pool_mode_t;
+
+/* Pooling on quantized NHWC values with input and output sharing (scale, zero point), as the
+ * frontend enforces.  Padding taps are excluded (reading R20):
+ *   MAX: out = max over the valid taps;
+ *   AVG: s = sum over the valid taps (int32), n = their count,
+ *        out = sign(s) * floor((2|s| + n) / (2n))   (rounding division, ties away from zero).
+ * Output is N x P x Q x C with P = (H + pad_t + pad_b - R)/stride_h + 1 (likewise Q).
+ * in_cstride / out_cstride: channel pitch of a pixel in elements (0 => C).  in, out: device. */
+typedef struct {
+  int32_t N, H, W, C, R, S;
+  int32_t stride_h, stride_w, pad_t, pad_l, pad_b, pad_r;
+  int32_t in_cstride, out_cstride;
+  qnn_dtype_t dtype;            /* QNN_U8 or QNN_S8 */
+  qnn_pool_mode_t mode;
+} qnn_pool2d_desc_t;
+QNN_API qnn_status_t qnn_pool2d(const qnn_pool2d_desc_t* d, const void* in, void* out, qnn_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

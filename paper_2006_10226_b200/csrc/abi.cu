@@ -1011,3 +1011,55 @@ qnn_status_t qnn_dequantize(const void* in, qnn_dtype_t in_dtype, float* out, co
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------- glue
+extern "C" QNN_API qnn_status_t qnn_add(const void* a, qnn_dtype_t a_dtype, float s_a, int32_t zp_a, const void* b,
+                                       qnn_dtype_t b_dtype, float s_b, int32_t zp_b, void* out,
+                                       qnn_dtype_t out_dtype, float s_out, int32_t zp_out, int64_t count,
+                                       qnn_rounding_t rounding, int32_t relu, qnn_stream_t stream) {
+  using namespace qnn;
+  if (!is_8bit(a_dtype) || !is_8bit(b_dtype) || !is_8bit(out_dtype)) return QNN_ERR_INVALID_VALUE;
+  if (!scale_ok(s_a) || !scale_ok(s_b) || !scale_ok(s_out)) return QNN_ERR_INVALID_VALUE;
+  if (!zp_ok(a_dtype, zp_a) || !zp_ok(b_dtype, zp_b) || !zp_ok(out_dtype, zp_out)) return QNN_ERR_INVALID_VALUE;
+  if (rounding != QNN_ROUND_UPWARD && rounding != QNN_ROUND_TONEAREST) return QNN_ERR_INVALID_VALUE;
+  if (count < 0) return QNN_ERR_INVALID_VALUE;
+  if (count == 0) return QNN_OK;
+  if (!a || !b || !out) return QNN_ERR_INVALID_VALUE;
+  AddParams p{};
+  if (!kernel_multiplier((double)s_a / (double)s_out, &p.Ma, &p.ra) ||
+      !kernel_multiplier((double)s_b / (double)s_out, &p.Mb, &p.rb))
+    return QNN_ERR_UNSUPPORTED;
+  p.a = a; p.b = b; p.out = out; p.count = count;
+  p.vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) &
+           15) == 0;
+  p.a_s8 = a_dtype == QNN_S8; p.b_s8 = b_dtype == QNN_S8; p.o_s8 = out_dtype == QNN_S8;
+  p.zp_a = zp_a; p.zp_b = zp_b; p.zp_out = zp_out;
+  p.mode = (int)rounding; p.relu = relu != 0;
+  return cuda_status(launch_add(p, (cudaStream_t)stream));
+}
+
+extern "C" QNN_API qnn_status_t qnn_pool2d(const qnn_pool2d_desc_t* d, const void* in, void* out,
+                                          qnn_stream_t stream) {
+  using namespace qnn;
+  if (!d) return QNN_ERR_INVALID_VALUE;
+  if (d->N <= 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->R <= 0 || d->S <= 0 || d->stride_h <= 0 ||
+      d->stride_w <= 0 || d->pad_t < 0 || d->pad_l < 0 || d->pad_b < 0 || d->pad_r < 0)
+    return QNN_ERR_INVALID_VALUE;
+  if (!is_8bit(d->dtype) || (d->mode != QNN_POOL_MAX && d->mode != QNN_POOL_AVG)) return QNN_ERR_INVALID_VALUE;
+  if (d->pad_t >= d->R || d->pad_b >= d->R || d->pad_l >= d->S || d->pad_r >= d->S) return QNN_ERR_INVALID_VALUE;
+  const long long Hp = (long long)d->H + d->pad_t + d->pad_b, Wp = (long long)d->W + d->pad_l + d->pad_r;
+  if (Hp < d->R || Wp < d->S) return QNN_ERR_INVALID_VALUE;
+  PoolParams p{};
+  p.P = (int)((Hp - d->R) / d->stride_h + 1);
+  p.Q = (int)((Wp - d->S) / d->stride_w + 1);
+  p.in_cs = d->in_cstride ? d->in_cstride : d->C;
+  p.out_cs = d->out_cstride ? d->out_cstride : d->C;
+  if (p.in_cs < d->C || p.out_cs < d->C) return QNN_ERR_INVALID_VALUE;
+  if (!in || !out) return QNN_ERR_INVALID_VALUE;
+  p.in = in; p.out = out;
+  p.N = d->N; p.H = d->H; p.W = d->W; p.C = d->C; p.R = d->R; p.S = d->S;
+  p.sh = d->stride_h; p.sw = d->stride_w; p.pt = d->pad_t; p.pl = d->pad_l;
+  p.s8 = d->dtype == QNN_S8;
+  p.avg = d->mode == QNN_POOL_AVG;
+  return cuda_status(launch_pool(p, (cudaStream_t)stream));
+}

@@ -1,0 +1,175 @@
+// glue.cu — inter-layer glue on the int8 path: qnn.add and pooling.
+//
+//   qnn.add   (reading R19): y = sat(max?(zp_out + R((a - zp_a) m_a) + R((b - zp_b) m_b)))
+//             with m_x = s_x / s_out as fixed-point multipliers (Eq. 5).
+//   pool2d    (reading R20): max, or rounding-division average, over the valid
+//             taps of each window; input and output share (scale, zero point).
+// Both are HBM-bound: 16-byte vector accesses, one warp instruction per contiguous span.
+#include "common.cuh"
+#include "internal.h"
+
+namespace qnn {
+
+namespace {
+
+__device__ __forceinline__ uint32_t pack4_sat_u8(int a, int b, int c, int d) {
+  uint32_t o;
+  asm("{\n\t.reg .u32 t;\n\tcvt.pack.sat.u8.s32.b32 t, %4, %3, 0;\n\tcvt.pack.sat.u8.s32.b32 %0, %2, %1, t;\n\t}"
+      : "=r"(o) : "r"(a), "r"(b), "r"(c), "r"(d));
+  return o;
+}
+__device__ __forceinline__ uint32_t pack4_sat_s8(int a, int b, int c, int d) {
+  uint32_t o;
+  asm("{\n\t.reg .u32 t;\n\tcvt.pack.sat.s8.s32.b32 t, %4, %3, 0;\n\tcvt.pack.sat.s8.s32.b32 %0, %2, %1, t;\n\t}"
+      : "=r"(o) : "r"(a), "r"(b), "r"(c), "r"(d));
+  return o;
+}
+template <bool S8>
+__device__ __forceinline__ int32_t byte_of(uint32_t w, int j) {
+  const uint32_t b = (w >> (8 * j)) & 0xFFu;
+  return S8 ? (int32_t)(int8_t)b : (int32_t)b;
+}
+
+// R((x - zp) * M * 2^-rsh): 64-bit fast form when rsh is in [11, 52] (|x - zp| < 2^9),
+// else the generic rounding of common.cuh.
+__device__ __forceinline__ int32_t rq_small(int32_t xz, int32_t M, int rsh, int mode) {
+  return (int32_t)rq_round((int64_t)xz * M, rsh, mode);
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------------- qnn.add
+template <bool AS8, bool BS8, bool OS8>
+__global__ void __launch_bounds__(256) add_kernel(const __grid_constant__ AddParams p) {
+  const long long nthreads = (long long)gridDim.x * blockDim.x;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nvec = p.vec ? p.count >> 4 : 0;
+  auto one = [&](int32_t a, int32_t b) -> int32_t {
+    int32_t y = rq_small(a - p.zp_a, p.Ma, p.ra, p.mode) + rq_small(b - p.zp_b, p.Mb, p.rb, p.mode) + p.zp_out;
+    if (p.relu) y = max(y, p.zp_out);
+    return y;
+  };
+  for (long long v = tid; v < nvec; v += nthreads) {
+    const uint4 av = __ldg(reinterpret_cast<const uint4*>(p.a) + v);
+    const uint4 bv = __ldg(reinterpret_cast<const uint4*>(p.b) + v);
+    const uint32_t aw[4] = {av.x, av.y, av.z, av.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+    uint32_t ow[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int32_t y[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = one(byte_of<AS8>(aw[k], j), byte_of<BS8>(bw[k], j));
+      ow[k] = OS8 ? pack4_sat_s8(y[0], y[1], y[2], y[3]) : pack4_sat_u8(y[0], y[1], y[2], y[3]);
+    }
+    reinterpret_cast<uint4*>(p.out)[v] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+  }
+  for (long long i = (nvec << 4) + tid; i < p.count; i += nthreads) {
+    const uint8_t* a8 = reinterpret_cast<const uint8_t*>(p.a);
+    const uint8_t* b8 = reinterpret_cast<const uint8_t*>(p.b);
+    const int32_t a = AS8 ? (int32_t)(int8_t)a8[i] : (int32_t)a8[i];
+    const int32_t b = BS8 ? (int32_t)(int8_t)b8[i] : (int32_t)b8[i];
+    const int32_t y = min(max(one(a, b), OS8 ? -128 : 0), OS8 ? 127 : 255);
+    reinterpret_cast<uint8_t*>(p.out)[i] = (uint8_t)y;
+  }
+}
+
+cudaError_t launch_add(const AddParams& p, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = p.vec ? (p.count + 15) / 16 : p.count;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)sms * 8));
+#define QNN_ADD(A_, B_, O_) \
+  if (p.a_s8 == A_ && p.b_s8 == B_ && p.o_s8 == O_) add_kernel<A_, B_, O_><<<blocks, 256, 0, s>>>(p);
+  QNN_ADD(false, false, false) QNN_ADD(false, false, true) QNN_ADD(false, true, false) QNN_ADD(false, true, true)
+  QNN_ADD(true, false, false) QNN_ADD(true, false, true) QNN_ADD(true, true, false) QNN_ADD(true, true, true)
+#undef QNN_ADD
+  count_launch();
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------------- pooling
+// VEC channels per thread (16: one uint4 per tap, C % 16 == 0 and aligned pitches; else 1).
+template <int VEC, bool S8, bool AVG>
+__global__ void __launch_bounds__(256) pool_kernel(const __grid_constant__ PoolParams p) {
+  const int G = p.C / VEC;
+  const long long total = (long long)p.N * p.P * p.Q * G;
+  const uint8_t* in = reinterpret_cast<const uint8_t*>(p.in);
+  uint8_t* out = reinterpret_cast<uint8_t*>(p.out);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(idx % G);
+    const long long pix = idx / G;
+    const int q = (int)(pix % p.Q);
+    const long long t = pix / p.Q;
+    const int pp = (int)(t % p.P), n = (int)(t / p.P);
+    int32_t acc[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] = AVG ? 0 : INT32_MIN;
+    int cnt = 0;
+    for (int r = 0; r < p.R; ++r) {
+      const int h = pp * p.sh + r - p.pt;
+      if (h < 0 || h >= p.H) continue;
+      for (int s = 0; s < p.S; ++s) {
+        const int w = q * p.sw + s - p.pl;
+        if (w < 0 || w >= p.W) continue;
+        ++cnt;
+        const uint8_t* src = in + (((long long)n * p.H + h) * p.W + w) * p.in_cs + g * VEC;
+        if (VEC == 16) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+          const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int32_t x = byte_of<S8>(vw[j >> 2], j & 3);
+            acc[j] = AVG ? acc[j] + x : max(acc[j], x);
+          }
+        } else {
+          const int32_t x = S8 ? (int32_t)(int8_t)src[0] : (int32_t)src[0];
+          acc[0] = AVG ? acc[0] + x : max(acc[0], x);
+        }
+      }
+    }
+    int32_t y[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      if (AVG) {
+        // sign(s) * floor((2|s| + n) / (2n)); all operands are small positive ints
+        const int32_t a = acc[j] < 0 ? -acc[j] : acc[j];
+        const int32_t m = cnt > 0 ? (2 * a + cnt) / (2 * cnt) : 0;
+        y[j] = acc[j] < 0 ? -m : m;
+      } else {
+        y[j] = cnt > 0 ? acc[j] : 0;
+      }
+    }
+    uint8_t* dst = out + (((long long)n * p.P + pp) * p.Q + q) * p.out_cs + g * VEC;
+    if (VEC == 16) {
+      uint32_t ow[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        ow[k] = S8 ? pack4_sat_s8(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3])
+                   : pack4_sat_u8(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    } else {
+      dst[0] = (uint8_t)y[0];
+    }
+  }
+}
+
+cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool v16 = p.C % 16 == 0 && p.in_cs % 16 == 0 && p.out_cs % 16 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(p.in) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
+  const long long total = (long long)p.N * p.P * p.Q * (v16 ? p.C / 16 : p.C);
+  const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)sms * 16));
+#define QNN_POOL(V_, S_, A_) \
+  if ((v16 ? 16 : 1) == V_ && p.s8 == S_ && p.avg == A_) pool_kernel<V_, S_, A_><<<blocks, 256, 0, s>>>(p);
+  QNN_POOL(16, false, false) QNN_POOL(16, false, true) QNN_POOL(16, true, false) QNN_POOL(16, true, true)
+  QNN_POOL(1, false, false) QNN_POOL(1, false, true) QNN_POOL(1, true, false) QNN_POOL(1, true, true)
+#undef QNN_POOL
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace qnn

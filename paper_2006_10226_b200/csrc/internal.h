@@ -215,6 +215,31 @@ cudaError_t launch_requantize(const RequantParams& p, cudaStream_t s);
 cudaError_t launch_quantize(const QuantParams& p, cudaStream_t s);
 cudaError_t launch_dequantize(const QuantParams& p, cudaStream_t s);
 
+// ---------------------------------------------------------------------------
+// Glue (glue.cu): qnn.add, pooling
+// ---------------------------------------------------------------------------
+struct AddParams {
+  const void* a;
+  const void* b;
+  void* out;
+  long long count;
+  int vec;                      // 16-byte vector path (all three pointers 16-B aligned)
+  bool a_s8, b_s8, o_s8;
+  int32_t zp_a, zp_b, zp_out;
+  int32_t Ma, Mb;               // fixed-point multipliers of s_a/s_out, s_b/s_out
+  int ra, rb;                   // right shifts (31 - shift), 1..62
+  int mode, relu;
+};
+cudaError_t launch_add(const AddParams& p, cudaStream_t s);
+struct PoolParams {
+  const void* in;
+  void* out;
+  long long in_cs, out_cs;
+  int N, H, W, C, P, Q, R, S, sh, sw, pt, pl;
+  bool s8, avg;
+};
+cudaError_t launch_pool(const PoolParams& p, cudaStream_t s);
+
 // launch accounting (abi.cu)
 void count_launch(int n = 1);
 

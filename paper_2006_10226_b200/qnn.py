@@ -33,11 +33,17 @@ EXPORTED = ["qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset
             "qnn_conv2d_prepack_size", "qnn_conv2d_prepack", "qnn_conv2d_workspace_size", "qnn_conv2d_packed",
             "qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense_prepack_size", "qnn_dense_prepack",
             "qnn_dense_workspace_size", "qnn_dense_packed", "qnn_dense", "qnn_requantize", "qnn_quantize",
-            "qnn_dequantize"]
+            "qnn_dequantize", "qnn_add", "qnn_pool2d"]
 
 
 class QnnError(RuntimeError):
     pass
+
+
+class Pool2dDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("N", "H", "W", "C", "R", "S", "stride_h", "stride_w", "pad_t",
+                                               "pad_l", "pad_b", "pad_r", "in_cstride", "out_cstride")] + \
+               [("dtype", ctypes.c_int), ("mode", ctypes.c_int)]
 
 
 class OutputParams(ctypes.Structure):
@@ -98,6 +104,10 @@ def lib() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
             L.qnn_dequantize.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(i64), i32, i32,
                                          ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
+            f32 = ctypes.c_float
+            L.qnn_add.argtypes = [vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32,
+                                  i64, ctypes.c_int, i32, vp]
+            L.qnn_pool2d.argtypes = [ctypes.POINTER(Pool2dDesc), vp, vp, vp]
             for name in EXPORTED:
                 if name not in ("qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset"):
                     getattr(L, name).restype = ctypes.c_int
@@ -324,4 +334,34 @@ def qnn_dequantize(q: torch.Tensor, scales, zero_points, axis=-1, out=None, stre
         sc = _floats([sc[0]] * len(zp))
     _check(lib().qnn_dequantize(_dev(q, "q"), _TORCH_DT[q.dtype], _dev(out, "out"), shp, nd, int(axis), sc, zp,
                                 len(sc), ctypes.c_void_p(_stream(stream))), "qnn_dequantize")
+    return out
+
+
+# --------------------------------------------------------------------------- glue
+def qnn_add(a: torch.Tensor, s_a: float, zp_a: int, b: torch.Tensor, s_b: float, zp_b: int, s_out: float,
+            zp_out: int, out_dtype="u8", rounding="upward", relu=False, out=None, stream=None) -> torch.Tensor:
+    """qnn.add of two 8-bit tensors (same shape), requantized to (s_out, zp_out) (reading R19)."""
+    if a.shape != b.shape:
+        raise QnnError("qnn_add: shapes differ")
+    odt = _dtcode(out_dtype)
+    if out is None:
+        out = torch.empty(a.shape, dtype=_DT_TORCH[odt], device=a.device)
+    _check(lib().qnn_add(_dev(a, "a"), _TORCH_DT[a.dtype], float(s_a), int(zp_a), _dev(b, "b"), _TORCH_DT[b.dtype],
+                         float(s_b), int(zp_b), _dev(out, "out"), odt, float(s_out), int(zp_out), a.numel(),
+                         ROUNDING[rounding], int(bool(relu)), ctypes.c_void_p(_stream(stream))), "qnn_add")
+    return out
+
+
+def qnn_pool2d(x: torch.Tensor, mode: str, R: int, S: int, stride=(1, 1), pad=(0, 0, 0, 0), out=None,
+               stream=None) -> torch.Tensor:
+    """Max / average pooling of an NHWC 8-bit tensor (padding excluded, reading R20)."""
+    N, H, W, C = x.shape
+    d = Pool2dDesc(N, H, W, C, R, S, stride[0], stride[1], pad[0], pad[1], pad[2], pad[3], 0, 0,
+                   _TORCH_DT[x.dtype], 0 if mode == "max" else 1)
+    P = (H + pad[0] + pad[2] - R) // stride[0] + 1
+    Q = (W + pad[1] + pad[3] - S) // stride[1] + 1
+    if out is None:
+        out = torch.empty((N, P, Q, C), dtype=x.dtype, device=x.device)
+    _check(lib().qnn_pool2d(ctypes.byref(d), _dev(x, "x"), _dev(out, "out"), ctypes.c_void_p(_stream(stream))),
+           "qnn_pool2d")
     return out

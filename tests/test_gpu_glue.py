@@ -1,0 +1,67 @@
+"""GPU parity: qnn.add and pooling vs the oracle, bit-exact."""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_2006_10226_b200 import qnn
+    qnn.lib()
+    return qnn
+
+
+@pytest.mark.parametrize("adt,bdt,odt", [("u8", "u8", "u8"), ("u8", "s8", "s8"), ("s8", "s8", "u8")])
+@pytest.mark.parametrize("mode", ["upward", "tonearest"])
+@pytest.mark.parametrize("relu", [False, True])
+def test_add(q, adt, bdt, odt, mode, relu):
+    g = np.random.default_rng(zlib.crc32(f"{adt}{bdt}{odt}{mode}{relu}".encode()))
+    for n in (1, 15, 16, 4097, 256 * 56 * 56):
+        a = gen.rand_q(g, (n,), adt)
+        b = gen.rand_q(g, (n,), bdt)
+        s_a, s_b, s_o = (float(np.float32(v)) for v in g.uniform(0.01, 0.3, 3))
+        za = int(g.integers(0, 256)) if adt == "u8" else int(g.integers(-128, 128))
+        zb = int(g.integers(0, 256)) if bdt == "u8" else int(g.integers(-128, 128))
+        zo = int(g.integers(0, 256)) if odt == "u8" else int(g.integers(-128, 128))
+        want = orc.add(a, s_a, za, b, s_b, zb, s_o, zo, odt, mode, relu)
+        got = q.qnn_add(torch.from_numpy(a).cuda(), s_a, za, torch.from_numpy(b).cuda(), s_b, zb, s_o, zo, odt,
+                        mode, relu).cpu().numpy()
+        assert np.array_equal(got, want), (n, np.argwhere(got != want)[:5])
+
+
+def test_add_unaligned(q):
+    g = np.random.default_rng(5)
+    base_a = torch.from_numpy(gen.rand_q(g, (5000,), "u8")).cuda()
+    base_b = torch.from_numpy(gen.rand_q(g, (5000,), "u8")).cuda()
+    a, b = base_a[3:3 + 4001], base_b[7:7 + 4001]
+    want = orc.add(a.cpu().numpy(), 0.05, 3, b.cpu().numpy(), 0.07, 200, 0.1, 128, "u8")
+    got = q.qnn_add(a, 0.05, 3, b, 0.07, 200, 0.1, 128, "u8").cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+POOLS = [
+    # N, H, W, C, R, S, stride, pad, mode, dtype
+    (2, 112, 112, 64, 3, 3, (2, 2), (1, 1, 1, 1), "max", "u8"),     # ResNet-50 stem max pool
+    (4, 7, 7, 2048, 7, 7, (1, 1), (0, 0, 0, 0), "avg", "u8"),       # ResNet-50 global average pool
+    (2, 8, 8, 2048, 8, 8, (1, 1), (0, 0, 0, 0), "avg", "s8"),       # Inception-v3 global pool
+    (2, 35, 35, 48, 3, 3, (1, 1), (1, 1, 1, 1), "avg", "u8"),       # Inception branch pool, padded
+    (1, 13, 11, 5, 3, 2, (2, 1), (1, 0, 1, 1), "max", "s8"),        # odd shapes: scalar path
+    (1, 9, 9, 7, 2, 2, (2, 2), (0, 0, 1, 1), "avg", "s8"),
+]
+
+
+@pytest.mark.parametrize("cfg", POOLS, ids=lambda c: f"{c[8]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}{c[5]}")
+def test_pool(q, cfg):
+    N, H, W, C, R, S, st, pad, mode, dt = cfg
+    g = np.random.default_rng(zlib.crc32(str(cfg).encode()))
+    x = gen.rand_q(g, (N, H, W, C), dt)
+    want = orc.pool2d(np.ascontiguousarray(x.transpose(0, 3, 1, 2)), mode, R, S, st, pad).transpose(0, 2, 3, 1)
+    got = q.qnn_pool2d(torch.from_numpy(x).cuda(), mode, R, S, st, pad).cpu().numpy()
+    assert np.array_equal(got, want)
