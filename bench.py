@@ -139,6 +139,134 @@ class GpuResNet50:
         self.graph.replay()
 
 
+# ----------------------------------------------------------------------------- full network (f1)
+def resnet50_full_model(batch: int, seed: int = 5000):
+    """Synthetic pre-quantized ResNet-50 as a true forward: the 53 convs of
+    resnet50_model's recipe plus the glue between them -- stem max pool, the 16 residual
+    qnn.add (+ ReLU), global average pool -- feeding the fc.  Add outputs use zp 0 (post-ReLU)
+    and scale 1.2 x the larger input scale."""
+    from workloads import gen
+    from workloads.shapes import resnet50_convs, resnet50_fc
+    img_scale, img_zp = float(np.float32(4.77 / 255)), 128
+    convs, q = {}, {}
+    for li, c in enumerate(resnet50_convs()):
+        convs[c.name] = c
+    layers = {}
+
+    def conv(name, zp_A, s_A, li):
+        c = convs[name]
+        g = gen.rng(seed + li)
+        W = gen.rand_q(g, (c.K, c.R, c.S, c.C), "s8", -127, 127)
+        kk = c.C * c.R * c.S
+        unit = gen.calibrated_out_scale(kk, (0, 255), zp_A, (-127, 127), 0, 1.0, 1.0)
+        s_W = (g.uniform(0.5, 1.5, size=c.K) / unit).astype(np.float32)
+        bias = g.integers(-4096, 4097, size=c.K).astype(np.int32)
+        s_out = gen.calibrated_out_scale(kk, (0, 255), zp_A, (-127, 127), 0, s_A, float(np.median(s_W)))
+        zp_out = 0 if c.relu else 128
+        layers[name] = dict(c=c, W=W, bias=bias, zp_A=zp_A, s_A=s_A, s_W=s_W,
+                            out=dict(scale=s_out, zero_point=zp_out, dtype="u8", rounding="upward", relu=c.relu))
+        return zp_out, s_out
+
+    li = 0
+    zp, s = conv("conv1", img_zp, img_scale, li)
+    blocks = []
+    x_q = (zp, s)       # max pool keeps the quantization
+    for name in [n for n in convs if n.endswith(".conv1") and n.startswith("layer")]:
+        pre = name[:-len(".conv1")]
+        li += 1
+        c1 = conv(pre + ".conv1", x_q[0], x_q[1], li)
+        li += 1
+        c2 = conv(pre + ".conv2", c1[0], c1[1], li)
+        li += 1
+        c3 = conv(pre + ".conv3", c2[0], c2[1], li)
+        sc = x_q
+        if pre + ".downsample" in convs:
+            li += 1
+            sc = conv(pre + ".downsample", x_q[0], x_q[1], li)
+        s_y = float(np.float32(1.2 * max(c3[1], sc[1])))
+        blocks.append(dict(name=pre, sc=sc, c3=c3, y=(0, s_y), down=pre + ".downsample" in convs))
+        x_q = (0, s_y)
+    fin, fout = resnet50_fc()
+    g = gen.rng(seed + 99)
+    fc = dict(zp_A=x_q[0], s_A=x_q[1], W=gen.rand_q(g, (fout, fin), "s8", -127, 127),
+              s_W=g.uniform(0.002, 0.02, size=fout).astype(np.float32),
+              bias=g.integers(-4096, 4097, size=fout).astype(np.int32))
+    image = gen.rng(seed + 98).standard_normal((batch, 224, 224, 3)).astype(np.float32)
+    return dict(layers=layers, blocks=blocks, fc=fc, image=image, img_scale=img_scale, img_zp=img_zp, batch=batch)
+
+
+class GpuResNet50Full:
+    """The full forward on the library's ops, captured as one CUDA graph."""
+
+    def __init__(self, m, dev):
+        import torch
+
+        from paper_2006_10226_b200 import qnn
+        self.torch, self.qnn, self.m = torch, qnn, m
+        B = m["batch"]
+        self.ops, self.buf = {}, {}
+        for name, L in m["layers"].items():
+            c = L["c"]
+            op = qnn.PackedConv2d(B, c.H, c.W, c.C, torch.from_numpy(L["W"]).to(dev), torch.from_numpy(L["bias"]).to(dev),
+                                  L["zp_A"], 0, L["s_A"], L["s_W"], L["out"], c.stride, c.pad, (1, 1), 1)
+            self.ops[name] = op
+            self.buf[name] = torch.empty(op.out_shape(), dtype=op.out_dtype, device=dev)
+        self.image_d = torch.from_numpy(m["image"]).to(dev)
+        self.q_image = torch.empty(self.image_d.shape, dtype=torch.uint8, device=dev)
+        self.pool = torch.empty((B, 56, 56, 64), dtype=torch.uint8, device=dev)
+        for b in m["blocks"]:
+            self.buf[b["name"] + ".out"] = torch.empty_like(self.buf[b["name"] + ".conv3"])
+        self.gap = torch.empty((B, 1, 1, 2048), dtype=torch.uint8, device=dev)
+        fc = m["fc"]
+        self.fc = qnn.PackedDense(B, torch.from_numpy(fc["W"]).to(dev), torch.from_numpy(fc["bias"]).to(dev),
+                                  fc["zp_A"], 0, fc["s_A"], fc["s_W"], None)
+        self.fc_out = torch.empty((B, fc["W"].shape[0]), dtype=torch.int32, device=dev)
+        self.logit_scale = (np.float32(fc["s_A"]) * fc["s_W"].astype(np.float32)).astype(np.float32)
+        self.logits = torch.empty(self.fc_out.shape, dtype=torch.float32, device=dev)
+        self.graph = None
+
+    def step(self):
+        q, m = self.qnn, self.m
+        q.qnn_quantize(self.image_d, [m["img_scale"]], [m["img_zp"]], "u8", out=self.q_image)
+        self.ops["conv1"](self.q_image, out=self.buf["conv1"])
+        q.qnn_pool2d(self.buf["conv1"], "max", 3, 3, (2, 2), (1, 1, 1, 1), out=self.pool)
+        x = self.pool
+        for b in m["blocks"]:
+            n = b["name"]
+            self.ops[n + ".conv1"](x, out=self.buf[n + ".conv1"])
+            self.ops[n + ".conv2"](self.buf[n + ".conv1"], out=self.buf[n + ".conv2"])
+            self.ops[n + ".conv3"](self.buf[n + ".conv2"], out=self.buf[n + ".conv3"])
+            sc = x
+            if b["down"]:
+                self.ops[n + ".downsample"](x, out=self.buf[n + ".downsample"])
+                sc = self.buf[n + ".downsample"]
+            c3q, scq, yq = b["c3"], b["sc"], b["y"]
+            q.qnn_add(self.buf[n + ".conv3"], c3q[1], c3q[0], sc, scq[1], scq[0], yq[1], yq[0], "u8", "upward",
+                      relu=True, out=self.buf[n + ".out"])
+            x = self.buf[n + ".out"]
+        q.qnn_pool2d(x, "avg", 7, 7, out=self.gap)
+        self.fc(self.gap.view(self.gap.shape[0], -1), out=self.fc_out)
+        q.qnn_dequantize(self.fc_out, self.logit_scale, [0], axis=-1, out=self.logits)
+
+    def capture(self):
+        torch = self.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        self.qnn.launch_counter_reset()
+        with torch.cuda.graph(self.graph):
+            self.step()
+        self.launches_per_step = self.qnn.launch_counter()
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
@@ -208,6 +336,35 @@ def oracle_forward(model, n_img: int = 1):
     return orc.dequantize(acc, scale, [0], axis=-1), outs
 
 
+def oracle_full_forward(m, n_img: int = 1):
+    """The oracle on the full forward of resnet50_full_model (NHWC in/out at each op)."""
+    import oracle as orc
+    nchw = lambda t: np.ascontiguousarray(t.transpose(0, 3, 1, 2))
+    nhwc = lambda t: np.ascontiguousarray(t.transpose(0, 2, 3, 1))
+
+    def conv(name, x):
+        L = m["layers"][name]
+        c = L["c"]
+        y = orc.qnn_conv2d(nchw(x), nchw(L["W"]), L["zp_A"], 0, L["s_A"], L["s_W"], L["bias"], L["out"], c.stride,
+                           c.pad)
+        return nhwc(y)
+
+    x = orc.quantize(m["image"][:n_img], [m["img_scale"]], [m["img_zp"]], "u8")
+    x = conv("conv1", x)
+    x = nhwc(orc.pool2d(nchw(x), "max", 3, 3, (2, 2), (1, 1, 1, 1)))
+    for b in m["blocks"]:
+        n = b["name"]
+        y = conv(n + ".conv3", conv(n + ".conv2", conv(n + ".conv1", x)))
+        sc = conv(n + ".downsample", x) if b["down"] else x
+        (zc, sc3), (zs, ss), (zy, sy) = b["c3"], b["sc"], b["y"]
+        x = orc.add(y, sc3, zc, sc, ss, zs, sy, zy, "u8", "upward", relu=True)
+    x = nhwc(orc.pool2d(nchw(x), "avg", 7, 7))
+    fc = m["fc"]
+    acc = orc.qnn_dense(x.reshape(x.shape[0], -1), fc["W"], fc["zp_A"], 0, fc["s_A"], fc["s_W"], fc["bias"], None)
+    scale = (np.float32(fc["s_A"]) * fc["s_W"]).astype(np.float32)
+    return orc.dequantize(acc, scale, [0], axis=-1)
+
+
 def cpu_baseline(model, n_img: int = 1):
     import oracle as orc
     t0 = time.perf_counter()
@@ -252,6 +409,8 @@ def main():
     ap.add_argument("--impl", default="qnn", choices=["qnn", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown-steps", type=int, default=5)
+    ap.add_argument("--no-full-network", dest="full_network", action="store_false",
+                    help="skip the full-forward (glue ops) measurement")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "contract: at least 3 warm-up steps"
 
@@ -348,7 +507,23 @@ def main():
     fc_ms /= args.breakdown_steps
     macs = [sp.macs() for sp in net.stack.specs]
     fc_macs = model["fc"]["A"].shape[0] * model["fc"]["W"].shape[0] * model["fc"]["W"].shape[1]
-    gemm_ms = float(layer_ms.sum() + fc_ms)
+    # GEMM time of a step: the 54 GEMM launches captured as ONE graph (exactly the step's
+    # kernels minus quantize/dequantize), replayed back to back between two events
+    gg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gg):
+        net.stack.run()
+        net.fc(net.fc_in, out=net.fc_out)
+    for _ in range(2):
+        gg.replay()
+    torch.cuda.synchronize()
+    reps = max(3, args.breakdown_steps)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    for _ in range(reps):
+        gg.replay()
+    g1.record()
+    torch.cuda.synchronize()
+    gemm_ms = g0.elapsed_time(g1) / reps
     gemm_ops = 2.0 * (sum(macs) + fc_macs)
     gemm_launches = nl + 1
     peaks = {}
@@ -368,6 +543,32 @@ def main():
         pass
     step_ops = 2.0 * (net.stack.total_macs() + fc_macs)
     conv_tops = step_ops / (ms_per_step / 1000.0) / 1e12
+
+    # ---------------- full network: the same convs plus max pool, 16 residual
+    # qnn.add and global average pool between them; reported alongside, not as `value`
+    full = None
+    if args.full_network:
+        fm = resnet50_full_model(args.batch)
+        fnet = GpuResNet50Full(fm, dev)
+        fnet.capture()
+        for _ in range(3):
+            fnet.replay()
+        torch.cuda.synchronize()
+        fsteps = max(3, min(args.steps, 50))
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(fsteps):
+            fnet.replay()
+        f1.record()
+        torch.cuda.synchronize()
+        fms = max_over_ranks(f0.elapsed_time(f1), dist if world > 1 else None, dev) / fsteps
+        full = {"value": round(args.batch * world / (fms / 1000.0), 1), "unit": "images/s",
+                "ms_per_step": round(fms, 4), "steps": fsteps, "launches_per_step": fnet.launches_per_step,
+                "ops": "quantize, conv1, max pool 3x3/2, 16 x (3-4 conv + qnn.add + ReLU), global avg pool, fc, "
+                       "dequantize"}
+        del fnet
 
     if rank != 0:
         if world > 1:
@@ -402,6 +603,7 @@ def main():
                      "ops_per_step": gemm_ops},
         "clocks": clk,
         "cpu_baseline": cpu,
+        "full_network": full,
         "layers": layers,
     }
     print(json.dumps(line), flush=True)
