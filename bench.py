@@ -140,11 +140,13 @@ class GpuResNet50:
 
 
 # ----------------------------------------------------------------------------- full network (f1)
-def resnet50_full_model(batch: int, seed: int = 5000):
+def resnet50_full_model(batch: int, seed: int = 5000, fused: bool = True):
     """Synthetic pre-quantized ResNet-50 as a true forward: the 53 convs of
     resnet50_model's recipe plus the glue between them -- stem max pool, the 16 residual
     qnn.add (+ ReLU), global average pool -- feeding the fc.  Add outputs use zp 0 (post-ReLU)
-    and scale 1.2 x the larger input scale."""
+    and scale 1.2 x the larger input scale.  fused: each residual add runs inside the block's
+    conv3 epilogue (qnn_conv2d_packed_add: conv3 requantized straight to the add's output
+    scale); else conv3 writes u8 and a separate qnn.add follows."""
     from workloads import gen
     from workloads.shapes import resnet50_convs, resnet50_fc
     img_scale, img_zp = float(np.float32(4.77 / 255)), 128
@@ -184,7 +186,9 @@ def resnet50_full_model(batch: int, seed: int = 5000):
             li += 1
             sc = conv(pre + ".downsample", x_q[0], x_q[1], li)
         s_y = float(np.float32(1.2 * max(c3[1], sc[1])))
-        blocks.append(dict(name=pre, sc=sc, c3=c3, y=(0, s_y), down=pre + ".downsample" in convs))
+        if fused:
+            layers[pre + ".conv3"]["out"] = dict(scale=s_y, zero_point=0, dtype="u8", rounding="upward", relu=True)
+        blocks.append(dict(name=pre, sc=sc, c3=c3, y=(0, s_y), down=pre + ".downsample" in convs, fused=fused))
         x_q = (0, s_y)
     fin, fout = resnet50_fc()
     g = gen.rng(seed + 99)
@@ -235,14 +239,18 @@ class GpuResNet50Full:
             n = b["name"]
             self.ops[n + ".conv1"](x, out=self.buf[n + ".conv1"])
             self.ops[n + ".conv2"](self.buf[n + ".conv1"], out=self.buf[n + ".conv2"])
-            self.ops[n + ".conv3"](self.buf[n + ".conv2"], out=self.buf[n + ".conv3"])
             sc = x
             if b["down"]:
                 self.ops[n + ".downsample"](x, out=self.buf[n + ".downsample"])
                 sc = self.buf[n + ".downsample"]
             c3q, scq, yq = b["c3"], b["sc"], b["y"]
-            q.qnn_add(self.buf[n + ".conv3"], c3q[1], c3q[0], sc, scq[1], scq[0], yq[1], yq[0], "u8", "upward",
-                      relu=True, out=self.buf[n + ".out"])
+            if b["fused"]:
+                self.ops[n + ".conv3"](self.buf[n + ".conv2"], out=self.buf[n + ".out"],
+                                       residual=(sc, scq[1], scq[0]))
+            else:
+                self.ops[n + ".conv3"](self.buf[n + ".conv2"], out=self.buf[n + ".conv3"])
+                q.qnn_add(self.buf[n + ".conv3"], c3q[1], c3q[0], sc, scq[1], scq[0], yq[1], yq[0], "u8", "upward",
+                          relu=True, out=self.buf[n + ".out"])
             x = self.buf[n + ".out"]
         q.qnn_pool2d(x, "avg", 7, 7, out=self.gap)
         self.fc(self.gap.view(self.gap.shape[0], -1), out=self.fc_out)
@@ -354,10 +362,16 @@ def oracle_full_forward(m, n_img: int = 1):
     x = nhwc(orc.pool2d(nchw(x), "max", 3, 3, (2, 2), (1, 1, 1, 1)))
     for b in m["blocks"]:
         n = b["name"]
-        y = conv(n + ".conv3", conv(n + ".conv2", conv(n + ".conv1", x)))
+        y2 = conv(n + ".conv2", conv(n + ".conv1", x))
         sc = conv(n + ".downsample", x) if b["down"] else x
         (zc, sc3), (zs, ss), (zy, sy) = b["c3"], b["sc"], b["y"]
-        x = orc.add(y, sc3, zc, sc, ss, zs, sy, zy, "u8", "upward", relu=True)
+        if b["fused"]:
+            L = m["layers"][n + ".conv3"]
+            c = L["c"]
+            x = nhwc(orc.qnn_conv2d_add(nchw(y2), nchw(L["W"]), L["zp_A"], 0, L["s_A"], L["s_W"], L["bias"],
+                                        nchw(sc), ss, zs, L["out"], c.stride, c.pad))
+        else:
+            x = orc.add(conv(n + ".conv3", y2), sc3, zc, sc, ss, zs, sy, zy, "u8", "upward", relu=True)
     x = nhwc(orc.pool2d(nchw(x), "avg", 7, 7))
     fc = m["fc"]
     acc = orc.qnn_dense(x.reshape(x.shape[0], -1), fc["W"], fc["zp_A"], 0, fc["s_A"], fc["s_W"], fc["bias"], None)
@@ -566,8 +580,8 @@ def main():
         fms = max_over_ranks(f0.elapsed_time(f1), dist if world > 1 else None, dev) / fsteps
         full = {"value": round(args.batch * world / (fms / 1000.0), 1), "unit": "images/s",
                 "ms_per_step": round(fms, 4), "steps": fsteps, "launches_per_step": fnet.launches_per_step,
-                "ops": "quantize, conv1, max pool 3x3/2, 16 x (3-4 conv + qnn.add + ReLU), global avg pool, fc, "
-                       "dequantize"}
+                "ops": "quantize, conv1, max pool 3x3/2, 16 x (3-4 conv, the residual qnn.add + ReLU fused into "
+                       "conv3's epilogue), global avg pool, fc, dequantize"}
         del fnet
 
     if rank != 0:

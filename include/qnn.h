@@ -166,6 +166,20 @@ QNN_API qnn_status_t qnn_conv2d_packed(const qnn_conv2d_desc_t* d, const qnn_out
                                const void* packed, const void* input, void* output,
                                void* workspace, size_t workspace_bytes, qnn_stream_t stream);
 
+/* qnn.conv2d fused with a residual qnn.add (reading R19): the conv's
+ * int32 result requantized to (s_out, 0) plus the residual requantized to (s_out, 0), then
+ * zp_out, ReLU (lower bound zp_out when o->relu), act clamps and saturation:
+ *   out = sat(zp_out + R(acc * m_k) + R((res - res_zp) * res_scale / s_out))
+ * `residual`: NHWC, N x P x Q x K (the conv output's shape), channel pitch res_cstride (0 => K),
+ * 8-bit (res_dtype S8/U8), base and pitch 16-byte aligned.  Requires requantized output (o not
+ * NULL), K % 32 == 0 and a non-depthwise conv (else UNSUPPORTED).  Everything else as
+ * qnn_conv2d_packed. */
+QNN_API qnn_status_t qnn_conv2d_packed_add(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o,
+                                           const void* packed, const void* input, const void* residual,
+                                           qnn_dtype_t res_dtype, float res_scale, int32_t res_zero_point,
+                                           int32_t res_cstride, void* output, void* workspace,
+                                           size_t workspace_bytes, qnn_stream_t stream);
+
 /* One-shot convenience: prepack into the front of `workspace`, then run.
  * workspace_bytes >= prepack_size (rounded up to 256) + workspace_size.
  * Not graph-capturable (prepack blocks). */

@@ -540,12 +540,33 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
   return cuda_status(e);
 }
 
+struct ResidualArgs {   // fused residual add (qnn_conv2d_packed_add)
+  const void* ptr;
+  qnn_dtype_t dtype;
+  float scale;
+  int32_t zp;
+  int32_t cstride;
+};
+
 static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, const void* packed,
-                                const void* input, void* output, void* ws, size_t ws_bytes, cudaStream_t s) {
+                                const void* input, void* output, void* ws, size_t ws_bytes, cudaStream_t s,
+                                const ResidualArgs* res = nullptr) {
   ConvPlan pl;
   qnn_status_t st = make_plan(d, o, pl, /*need_scales=*/false);
   if (st != QNN_OK) return st;
   if (!packed || !input || !output) return QNN_ERR_INVALID_VALUE;
+  int32_t res_M = 0, res_rsh = 1;
+  long long res_cs = 0;
+  if (res) {
+    if (!res->ptr || !o || !is_8bit(res->dtype) || !scale_ok(res->scale) || !zp_ok(res->dtype, res->zp))
+      return QNN_ERR_INVALID_VALUE;
+    res_cs = res->cstride ? res->cstride : d->K;
+    if (res_cs < d->K) return QNN_ERR_INVALID_VALUE;
+    if (pl.depthwise || d->K % 32 != 0) return QNN_ERR_UNSUPPORTED;
+    if ((reinterpret_cast<uintptr_t>(res->ptr) & 15) || (res_cs % 16)) return QNN_ERR_MISALIGNED;
+    if (!kernel_multiplier((double)res->scale / (double)o->output_scale, &res_M, &res_rsh))
+      return QNN_ERR_UNSUPPORTED;
+  }
   if (reinterpret_cast<uintptr_t>(packed) & 255) return QNN_ERR_MISALIGNED;
   if (pl.ws_total && (!ws || ws_bytes < pl.ws_total)) return QNN_ERR_WORKSPACE;
   if (ws && (reinterpret_cast<uintptr_t>(ws) & 255)) return QNN_ERR_MISALIGNED;
@@ -775,10 +796,20 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   ep.zp_out = pl.zp_out;
   ep.lo = pl.lo;
   ep.hi = pl.hi;
+  if (res) {
+    ep.res = reinterpret_cast<const uint8_t*>(res->ptr);
+    ep.res_pitch = res_cs;
+    ep.res_M = res_M;
+    ep.res_rsh = res_rsh;
+    ep.res_zp = res->zp;
+    ep.res_s8 = res->dtype == QNN_S8;
+  }
   const int tiles = pl.num_m * pl.num_n;
   const int grid = std::min(tiles, sm_count());
   int64_t qlo = INT32_MIN, qhi = INT32_MAX;
   if (pl.requant) dtype_range(pl.out_dt, &qlo, &qhi);
+  // the residual can push the sum past [lo, hi] even when those are the dtype bounds, but
+  // the saturating pack covers the dtype range; an explicit clamp is needed only inside it
   const bool clamp = pl.requant && (pl.lo > qlo || pl.hi < qhi);
   const int mode = pl.requant ? pl.mode : 2;
   return cuda_status(launch_gemm(tmA, tmB, tmC, p, mode, clamp, grid, s));
@@ -864,6 +895,14 @@ qnn_status_t qnn_conv2d_packed(const qnn_conv2d_desc_t* d, const qnn_output_para
                                const void* input, void* output, void* workspace, size_t workspace_bytes,
                                qnn_stream_t stream) {
   return conv_packed(d, o, packed, input, output, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+qnn_status_t qnn_conv2d_packed_add(const qnn_conv2d_desc_t* d, const qnn_output_params_t* o, const void* packed,
+                                   const void* input, const void* residual, qnn_dtype_t res_dtype, float res_scale,
+                                   int32_t res_zero_point, int32_t res_cstride, void* output, void* workspace,
+                                   size_t workspace_bytes, qnn_stream_t stream) {
+  const ResidualArgs r{residual, res_dtype, res_scale, res_zero_point, res_cstride};
+  return conv_packed(d, o, packed, input, output, workspace, workspace_bytes, (cudaStream_t)stream, &r);
 }
 
 qnn_status_t qnn_conv2d(const qnn_conv2d_desc_t* d, const void* input, const void* kernel, const int32_t* bias,

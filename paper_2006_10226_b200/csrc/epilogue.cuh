@@ -118,11 +118,24 @@ __device__ __forceinline__ int32_t rq1(int32_t v, int32_t M, int32_t t, int32_t 
 // One 32-column chunk of one row: offsets, requantize, clamp; packed to 8-bit words
 // (MODE 0/1) or kept as int32 (MODE 2, raw).  Parameters are read four columns per
 // broadcast LDS.128: mt = {M, t} pairs, cc = c, off = folded offsets.
-template <int MODE, bool CLAMP, bool FAST, bool S8OUT>
+// Fused residual add (reading R19): R((res - zp_res) * s_res / s_out) with
+// the residual's per-tensor fixed-point multiplier, added to the requantized conv value before
+// the output clamp.  |res - zp_res| <= 255, so the 64-bit product never overflows.
+struct ResTerm {
+  int32_t M, rsh, zp, mode, s8;
+};
+__device__ __forceinline__ int32_t res_val(const ResTerm& t, uint32_t word, int byte) {
+  const uint32_t b = (word >> (8 * byte)) & 0xFFu;
+  const int32_t x = (t.s8 ? (int32_t)(int8_t)b : (int32_t)b) - t.zp;
+  return (int32_t)rq_round((int64_t)x * t.M, t.rsh, t.mode);
+}
+
+template <int MODE, bool CLAMP, bool FAST, bool S8OUT, bool RES = false>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const int4* __restrict__ off4,
                                           const int4* __restrict__ mt4, const int4* __restrict__ c4,
                                           int32_t rterm, int32_t zp_out, int32_t lo, int32_t hi,
-                                          uint32_t (&w)[8], int32_t* y) {
+                                          uint32_t (&w)[8], int32_t* y, const uint32_t* rw = nullptr,
+                                          const ResTerm* rt = nullptr) {
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
     const int4 o = off4[q4];
@@ -139,6 +152,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const int4* _
       for (int u = 0; u < 4; ++u) {
         const int32_t vv = (int32_t)(v[q4 * 4 + u] + (uint32_t)offs[u] - (uint32_t)rterm);  // wrap-exact (R10)
         int32_t r = rq1<MODE, FAST>(vv, Ms[u], Ts[u], Cs[u], zp_out);
+        if (RES) r += res_val(*rt, rw[q4], u);
         if (CLAMP) r = min(max(r, lo), hi);
         yy[u] = r;
       }
@@ -154,10 +168,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const int4* _
 
 // UPWARD fast path for one 32-column chunk of one row (see the header): two
 // columns per LDS.128 of {M, t} pairs and per LDS.128 of K values.
-template <bool CLAMP, bool S8OUT, bool RT>
+template <bool CLAMP, bool S8OUT, bool RT, bool RES = false>
 __device__ __forceinline__ void epi_chunk_up(const uint32_t (&v)[32], const int4* __restrict__ mt4,
                                              const longlong2* __restrict__ k2, int32_t rterm, int32_t lo,
-                                             int32_t hi, uint32_t (&w)[8]) {
+                                             int32_t hi, uint32_t (&w)[8], const uint32_t* rw = nullptr,
+                                             const ResTerm* rt = nullptr) {
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
     int32_t yy[4];
@@ -174,6 +189,10 @@ __device__ __forceinline__ void epi_chunk_up(const uint32_t (&v)[32], const int4
       const unsigned long long p1 = (unsigned long long)((long long)v1 * mt.z) + (unsigned long long)kk.y;
       int32_t r0 = (int32_t)(p0 >> 32) >> mt.y;
       int32_t r1 = (int32_t)(p1 >> 32) >> mt.w;
+      if (RES) {
+        r0 += res_val(*rt, rw[q4], 2 * h);
+        r1 += res_val(*rt, rw[q4], 2 * h + 1);
+      }
       if (CLAMP) {
         r0 = min(max(r0, lo), hi);
         r1 = min(max(r1, lo), hi);

@@ -75,7 +75,7 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
   if (kInstrument && tr && blockIdx.x == 0) tr[slot] = clock64();
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     qnn_gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
@@ -403,6 +403,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int kEpiThreads = 32 * nepi;
     int cur_n = -1, tile_fast = 1;
     const bool has_rt = e.rowsum != nullptr;
+    constexpr bool has_res = RES && MODE != 2;   // fused residual add: its own instantiation
+    ResTerm rt_res{e.res_M, e.res_rsh, e.res_zp, MODE, e.res_s8};
     int m_blk = m_first, n_blk = n_first;
     if (nsets > 1) {   // single N tile: tile t is (t, 0)
       m_blk = blockIdx.x + set * gridDim.x;
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #ifdef QNN_EPI_NO_TWO
       const bool two = false;
 #else
-      const bool two = MODE == 0 && tile_fast && tma_st && !dbg && c_end - c_begin == 2;
+      const bool two = MODE == 0 && tile_fast && tma_st && !dbg && c_end - c_begin == 2 && !has_res;
 #endif
       if (two) {
         uint32_t va[32], vb[32];
@@ -541,26 +543,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int4* mt4 = reinterpret_cast<const int4*>(sMT + j * 32);      // 2 columns per int4
         uint32_t w[8];
         int32_t y[out8 ? 1 : 32];
+        uint32_t rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // residual bytes of this row's 32 columns
+        if (has_res && row_ok && k0 < p.Nout) {
+          const uint4* rp = reinterpret_cast<const uint4*>(e.res + (long long)row * e.res_pitch + k0);
+          const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+          rw[0] = r0.x; rw[1] = r0.y; rw[2] = r0.z; rw[3] = r0.w;
+          rw[4] = r1.x; rw[5] = r1.y; rw[6] = r1.z; rw[7] = r1.w;
+        }
         if (MODE == 0) {
           if (tile_fast) {
             const longlong2* k2 = reinterpret_cast<const longlong2*>(reinterpret_cast<const long long*>(sOff) +
                                                                      cls * offp + j * 32);
-            if (has_rt)
+            if (has_res) {
+              if (has_rt)
+                epi_chunk_up<CLAMP, S8OUT, true, true>(v, mt4, k2, rterm, lo, hi, w, rw, &rt_res);
+              else
+                epi_chunk_up<CLAMP, S8OUT, false, true>(v, mt4, k2, rterm, lo, hi, w, rw, &rt_res);
+            } else if (has_rt) {
               epi_chunk_up<CLAMP, S8OUT, true>(v, mt4, k2, rterm, lo, hi, w);
-            else
+            } else {
               epi_chunk_up<CLAMP, S8OUT, false>(v, mt4, k2, rterm, lo, hi, w);
+            }
           } else {
             // generic 64-bit rounding (shifts outside [33, 52]): int32 offsets straight from global memory
             const int4* off4 = reinterpret_cast<const int4*>(e.off + (size_t)cls * e.Kpad + k0);
-            epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, mt4, rterm, zp_out, lo, hi, w, y);
+            if (has_res)
+              epi_chunk<MODE, CLAMP, false, S8OUT, true>(v, off4, mt4, mt4, rterm, zp_out, lo, hi, w, y, rw, &rt_res);
+            else
+              epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, mt4, rterm, zp_out, lo, hi, w, y);
           }
         } else {
           const int4* off4 = reinterpret_cast<const int4*>(sOff + cls * offp + j * 32);
           const int4* c4 = reinterpret_cast<const int4*>(sCC + j * 32);
-          if (tile_fast)
+          if (has_res) {
+            if (tile_fast)
+              epi_chunk<MODE, CLAMP, true, S8OUT, true>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y, rw, &rt_res);
+            else
+              epi_chunk<MODE, CLAMP, false, S8OUT, true>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y, rw,
+                                                         &rt_res);
+          } else if (tile_fast) {
             epi_chunk<MODE, CLAMP, true, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
-          else
+          } else {
             epi_chunk<MODE, CLAMP, false, S8OUT>(v, off4, mt4, c4, rterm, zp_out, lo, hi, w, y);
+          }
         }
         if (dbg & 2) {
         } else if constexpr (out8) {
@@ -636,13 +661,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES>
 static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                   const GemmParams& p, int grid, cudaStream_t stream) {
   static int attr_done[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT>;
+  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT, RES>;
   if (dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
@@ -660,10 +685,13 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
                         int mode, bool clamp, int grid, cudaStream_t stream) {
   const bool cls = p.e.ncls > 1;
   const bool s8 = p.e.out_dtype == DT_S8;
-#define QNN_GEMM_CASE(M_, C_, K_, S_)                  \
-  if (mode == M_ && cls == C_ && clamp == K_ && s8 == S_) \
-    return launch_variant<M_, C_, K_, S_>(tmA, tmB, tmC, p, grid, stream);
-#define QNN_GEMM_CASES(M_, C_, K_) QNN_GEMM_CASE(M_, C_, K_, false) QNN_GEMM_CASE(M_, C_, K_, true)
+  const bool res = p.e.res != nullptr && mode != 2;
+#define QNN_GEMM_CASE(M_, C_, K_, S_, R_)                            \
+  if (mode == M_ && cls == C_ && clamp == K_ && s8 == S_ && res == R_) \
+    return launch_variant<M_, C_, K_, S_, R_>(tmA, tmB, tmC, p, grid, stream);
+#define QNN_GEMM_CASES(M_, C_, K_)                                                            \
+  QNN_GEMM_CASE(M_, C_, K_, false, false) QNN_GEMM_CASE(M_, C_, K_, true, false)              \
+  QNN_GEMM_CASE(M_, C_, K_, false, true) QNN_GEMM_CASE(M_, C_, K_, true, true)
   QNN_GEMM_CASES(0, false, false)
   QNN_GEMM_CASES(0, false, true)
   QNN_GEMM_CASES(0, true, false)
@@ -672,8 +700,8 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   QNN_GEMM_CASES(1, false, true)
   QNN_GEMM_CASES(1, true, false)
   QNN_GEMM_CASES(1, true, true)
-  QNN_GEMM_CASE(2, false, false, false)
-  QNN_GEMM_CASE(2, true, false, false)
+  QNN_GEMM_CASE(2, false, false, false, false)
+  QNN_GEMM_CASE(2, true, false, false, false)
 #undef QNN_GEMM_CASES
 #undef QNN_GEMM_CASE
   return cudaErrorInvalidValue;

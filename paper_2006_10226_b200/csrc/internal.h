@@ -34,6 +34,10 @@ struct GemmEpilogue {
   int out_dtype;           // DT_U8 / DT_S8 / DT_S32
   int tma_store;           // 8-bit output through per-warp TMA stores (pitch % 16 == 0)
   int32_t zp_out, lo, hi;  // lo/hi already include ReLU, act clamp and dtype range
+  // fused residual add (nullptr: none): + R((res - res_zp) * res_M * 2^-res_rsh) before the clamp
+  const uint8_t* res;
+  long long res_pitch;     // bytes between consecutive pixels of the residual
+  int32_t res_M, res_rsh, res_zp, res_s8;
 };
 
 // Division by a runtime divisor d >= 1 for dividends in [0, 2^31): q = umulhi(x, mul) >> shr

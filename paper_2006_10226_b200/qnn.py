@@ -33,7 +33,7 @@ EXPORTED = ["qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset
             "qnn_conv2d_prepack_size", "qnn_conv2d_prepack", "qnn_conv2d_workspace_size", "qnn_conv2d_packed",
             "qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense_prepack_size", "qnn_dense_prepack",
             "qnn_dense_workspace_size", "qnn_dense_packed", "qnn_dense", "qnn_requantize", "qnn_quantize",
-            "qnn_dequantize", "qnn_add", "qnn_pool2d"]
+            "qnn_dequantize", "qnn_add", "qnn_pool2d", "qnn_conv2d_packed_add"]
 
 
 class QnnError(RuntimeError):
@@ -108,6 +108,7 @@ def lib() -> ctypes.CDLL:
             L.qnn_add.argtypes = [vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32,
                                   i64, ctypes.c_int, i32, vp]
             L.qnn_pool2d.argtypes = [ctypes.POINTER(Pool2dDesc), vp, vp, vp]
+            L.qnn_conv2d_packed_add.argtypes = [cdp, odp, vp, vp, vp, ctypes.c_int, f32, i32, i32, vp, vp, sz, vp]
             for name in EXPORTED:
                 if name not in ("qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset"):
                     getattr(L, name).restype = ctypes.c_int
@@ -220,13 +221,22 @@ class PackedConv2d:
         d = self.desc
         return (d.N, self.P, self.Q, d.out_cstride or self.K)
 
-    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None, residual=None) -> torch.Tensor:
+        """Run the conv; residual=(tensor NHWC, scale, zero_point) fuses a qnn.add of it (reading R19)."""
         if out is None:
             out = torch.empty(self.out_shape(), dtype=self.out_dtype, device=x.device)
         ws = ctypes.c_void_p(self.workspace.data_ptr()) if self.workspace is not None else None
-        _check(lib().qnn_conv2d_packed(ctypes.byref(self.desc), self._op, ctypes.c_void_p(self.packed.data_ptr()),
-                                       _dev(x, "x"), _dev(out, "out"), ws, self.ws_bytes,
-                                       ctypes.c_void_p(_stream(stream))), "qnn_conv2d_packed")
+        if residual is None:
+            _check(lib().qnn_conv2d_packed(ctypes.byref(self.desc), self._op, ctypes.c_void_p(self.packed.data_ptr()),
+                                           _dev(x, "x"), _dev(out, "out"), ws, self.ws_bytes,
+                                           ctypes.c_void_p(_stream(stream))), "qnn_conv2d_packed")
+        else:
+            r, rs, rz = residual
+            _check(lib().qnn_conv2d_packed_add(ctypes.byref(self.desc), self._op,
+                                               ctypes.c_void_p(self.packed.data_ptr()), _dev(x, "x"),
+                                               _dev(r, "residual"), _TORCH_DT[r.dtype], float(rs), int(rz), 0,
+                                               _dev(out, "out"), ws, self.ws_bytes,
+                                               ctypes.c_void_p(_stream(stream))), "qnn_conv2d_packed_add")
         return out
 
 

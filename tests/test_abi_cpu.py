@@ -26,7 +26,7 @@ def _declared_symbols():
 
 def test_header_declares_abi():
     syms = _declared_symbols()
-    assert len(syms) == 20
+    assert len(syms) == 21
     for s in ("qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense", "qnn_requantize", "qnn_quantize", "qnn_dequantize"):
         assert s in syms
 

@@ -65,3 +65,33 @@ def test_pool(q, cfg):
     want = orc.pool2d(np.ascontiguousarray(x.transpose(0, 3, 1, 2)), mode, R, S, st, pad).transpose(0, 2, 3, 1)
     got = q.qnn_pool2d(torch.from_numpy(x).cuda(), mode, R, S, st, pad).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- conv + fused residual add
+FUSED = [
+    # N, C, H, W, K, R, stride, pad, res_dtype, out_dtype, relu, mode
+    (2, 64, 14, 14, 256, 1, (1, 1), (0, 0, 0, 0), "u8", "u8", True, "upward"),      # bottleneck conv3
+    (3, 32, 11, 13, 64, 3, (1, 1), (1, 1, 1, 1), "u8", "u8", True, "upward"),       # border classes
+    (2, 48, 9, 9, 96, 3, (2, 2), (1, 1, 1, 1), "s8", "s8", False, "tonearest"),
+    (1, 128, 7, 7, 512, 1, (1, 1), (0, 0, 0, 0), "u8", "u8", False, "upward"),      # 2 N tiles
+    (2, 16, 10, 10, 32, 3, (1, 1), (1, 1, 1, 1), "u8", "u8", True, "tonearest"),
+]
+
+
+@pytest.mark.parametrize("cfg", FUSED, ids=lambda c: f"C{c[1]}K{c[4]}_{c[2]}x{c[3]}_r{c[5]}_{c[8]}{c[9]}_{c[11]}")
+def test_conv_fused_residual_add(q, cfg):
+    from gpu_helpers import to_dev
+    N, C, H, W, K, R, st, pad, rdt, odt, relu, mode = cfg
+    case = gen.conv_case(1300 + C + K, N, C, H, W, K, R, R, st, pad, (1, 1), 1, "u8", "s8", out_dtype=odt,
+                         relu=relu, rounding=mode, zp_out=5 if odt == "u8" else -3)
+    P, Q = orc.out_hw(H, W, R, R, st, pad)
+    g = np.random.default_rng(zlib.crc32(str(cfg).encode()))
+    res = gen.rand_q(g, (N, P, Q, K), rdt)
+    s_res, zp_res = 0.7 * case.s_out, (117 if rdt == "u8" else -9)
+    op = q.PackedConv2d(N, H, W, C, to_dev(case.W), to_dev(case.bias), case.zp_A, case.zp_W, case.s_A, case.s_W,
+                        case.out_params(), case.stride, case.pad, (1, 1), 1)
+    y = op(to_dev(case.A), residual=(to_dev(res), s_res, zp_res)).cpu().numpy()
+    want = orc.qnn_conv2d_add(case.nchw(), case.oihw(), case.zp_A, case.zp_W, case.s_A, case.s_W, case.bias,
+                              np.ascontiguousarray(res.transpose(0, 3, 1, 2)), s_res, zp_res, case.out_params(),
+                              case.stride, case.pad).transpose(0, 2, 3, 1)
+    assert np.array_equal(y, want), (np.argwhere(y != want)[:5], y.size)

@@ -14,9 +14,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def test_resnet50_full_forward_matches_oracle():
+@pytest.mark.parametrize("fused", [True, False], ids=["fused_residual", "separate_add"])
+def test_resnet50_full_forward_matches_oracle(fused):
     import bench
-    m = bench.resnet50_full_model(2, seed=6100)
+    m = bench.resnet50_full_model(2, seed=6100, fused=fused)
     net = bench.GpuResNet50Full(m, torch.device("cuda"))
     net.step()
     torch.cuda.synchronize()
