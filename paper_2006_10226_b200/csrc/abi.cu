@@ -364,10 +364,27 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     pl.nchunks = (pl.Ct + best_bk - 1) / best_bk;
     pl.Cw = pl.nchunks * best_bk;
   }
-  pl.num_n = (d->K + 255) / 256;
-  pl.BN = round_up((d->K + pl.num_n - 1) / pl.num_n, 32);
-  pl.Kpad = pl.num_n * pl.BN;
   pl.num_m = (int)((pl.M + kGemmBM - 1) / kGemmBM);
+  {
+    // N tiling: fewest N tiles (BN <= 256) unless narrower tiles fill the persistent grid's last
+    // round better -- cost ~ rounds x (BN + 32), rounds = ceil(tiles / SMs) (wave quantisation of
+    // the small-M deep layers, e.g. ResNet-50 layer4 at batch 256: 196 tiles on 148 SMs)
+    const int sms = sm_count();
+    const int n0 = (d->K + 255) / 256;
+    long long best = -1;
+    for (int nn = n0; nn <= std::max(n0, (d->K + 63) / 64); ++nn) {
+      const int bn = round_up((d->K + nn - 1) / nn, 32);
+      if (bn < 64 && nn > n0) break;
+      const long long tiles = (long long)pl.num_m * nn;
+      const long long cost = (tiles + sms - 1) / sms * (bn + 32);
+      if (best < 0 || cost < best) {
+        best = cost;
+        pl.num_n = nn;
+        pl.BN = bn;
+      }
+    }
+  }
+  pl.Kpad = pl.num_n * pl.BN;
   pl.im2col = !(d->R == 1 && pl.gS == 1 && d->stride_h == 1 && pl.g_sw == 1 && d->pad_t == 0 && pl.g_pl == 0 &&
                  d->pad_b == 0 && pl.g_pr == 0);
   if (pl.im2col) {
