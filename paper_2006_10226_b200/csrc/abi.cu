@@ -1,3 +1,4 @@
+#include <cstdio>
 // abi.cu — the C ABI of libqnn.so (include/qnn.h): argument validation, the
 // host half of the paper's QNN canonicalisation — fixed-point
 // multiplier derivation, border-class tables, compile-time folding plans —
@@ -179,6 +180,8 @@ struct ConvPlan {
   bool a_build = false;  // fold done in shared memory by the GEMM's builder warps (no X' copy in HBM)
   int a_ib = 0, a_nr = 0, a_slot_bytes = 0, a_raw_bytes = 0;
   bool a_zpfill = false;  // a_build writes zp_A outside the image (single border class)
+  bool a_rows = false;    // stride-1 convs: staged input rows + per-tap descriptor offsets
+  int a_Wp = 0, a_T = 0, a_nri = 0, a_stage_bytes = 0;
   int Ct = 0;            // channel count / pitch seen by TMA
   // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
   int gW = 0, gS = 0, g_sw = 0, g_pl = 0, g_pr = 0, g_dw = 0;
@@ -455,6 +458,37 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       pl.stages = gemm_max_stages(pl.BK, pl.BN, 1, pl.b_res_kb, pl.kps, pl.a_raw_bytes);
     }
   }
+  // a_rows: stride-1 im2col convs with resident weights load the input rows a tile touches
+  // once per channel chunk and address every tap through the MMA descriptor (no per-tap
+  // im2col TMA); QNN_NO_AROWS=1 keeps the im2col path (A/B measurements)
+  static const bool no_arows = std::getenv("QNN_NO_AROWS") != nullptr;
+  if (!no_arows && pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && d->stride_h == 1 && d->stride_w == 1 &&
+      d->dil_h == 1 && d->dil_w == 1 && pl.num_n == 1 && pl.b_res_kb > 0 && d->C % pl.BK == 0) {
+    const int Wp = pl.Q + d->S - 1;
+    const long long flat = (long long)pl.P * Wp;
+    const int T = (int)((flat + kGemmBM - 1) / kGemmBM);
+    int nri = 0;
+    for (int t = 0; t < T; ++t) {
+      const long long f0 = (long long)t * kGemmBM, f1 = std::min(f0 + kGemmBM - 1, flat - 1);
+      nri = std::max(nri, (int)(f1 / Wp - f0 / Wp) + d->R);
+    }
+    const long long a_stage = ((long long)(nri * Wp + d->S) * pl.BK + 1023) / 1024 * 1024;
+    const int ncls = pl.ct.ncr * pl.ct.ncc;
+    const int num_kb = d->R * d->S * pl.nchunks;
+    if (Wp <= 256 && nri <= 256 && a_stage <= 96 * 1024) {
+      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb, d->R * d->S, 0, (int)a_stage);
+      if (st >= 2 && gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb, d->R * d->S, 0, (int)a_stage) <= 227 * 1024) {
+        pl.a_rows = true;
+        pl.a_Wp = Wp;
+        pl.a_T = T;
+        pl.a_nri = nri;
+        pl.a_stage_bytes = (int)a_stage;
+        pl.kps = d->R * d->S;
+        pl.stages = st;
+        pl.num_m = d->N * T;
+      }
+    }
+  }
   const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
@@ -485,6 +519,14 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     w = align256(w + (size_t)pl.M * 4);
   }
   pl.ws_total = w;
+  static const bool plan_trace = std::getenv("QNN_PLAN_TRACE") != nullptr;
+  if (plan_trace)
+    std::fprintf(stderr,
+                 "[qnn plan] N%d C%d %dx%d K%d %dx%d s%d: BK%d BN%d num_m%d num_n%d chunks%d stages%d kps%d b_res%d "
+                 "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB)\n",
+                 d->N, d->C, d->H, d->W, d->K, d->R, d->S, d->stride_h, pl.BK, pl.BN, pl.num_m, pl.num_n,
+                 pl.nchunks, pl.stages, pl.kps, pl.b_res_kb, (int)pl.im2col, (int)pl.fold, (int)pl.pad_copy,
+                 (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes);
   return QNN_OK;
 }
 
@@ -706,7 +748,19 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   bool ok;
   const int a_chan = (pl.pad_copy || pl.fold) ? pl.Ct : d->C;
   const int taps = d->R * pl.gS;
-  if (pl.a_build) {
+  if (pl.a_rows) {
+    // input (c, w, h, n), box = one channel chunk x Wp columns x a_nri rows, swizzled like the
+    // UMMA K-major layout of BK-byte rows; out-of-image pixels zero-filled (border classes)
+    const cuuint64_t dims[4] = {(cuuint64_t)d->C, (cuuint64_t)d->W, (cuuint64_t)d->H, (cuuint64_t)d->N};
+    const cuuint64_t strides[3] = {(cuuint64_t)pl.in_cs, (cuuint64_t)pl.in_cs * d->W,
+                                   (cuuint64_t)pl.in_cs * d->W * d->H};
+    const cuuint32_t box[4] = {(cuuint32_t)pl.BK, (cuuint32_t)pl.a_Wp, (cuuint32_t)pl.a_nri, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    ok = p_encode_tiled(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(input), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(pl.BK), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    small_tensor_fixup(&tmA, (uint64_t)pl.in_cs * d->W * d->H * d->N);
+  } else if (pl.a_build) {
     // raw input rows as (ib bytes, W*C/ib, H, N): one box = R filter rows of one output row
     const uint64_t rowlen = (uint64_t)d->W * d->C;
     const cuuint64_t dims[4] = {(cuuint64_t)pl.a_ib, rowlen / pl.a_ib, (cuuint64_t)d->H, (cuuint64_t)d->N};
@@ -734,7 +788,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   alignas(64) CUtensorMap tmC[4];
   std::memset(tmC, 0, sizeof(tmC));
   static const bool no_tma_store = std::getenv("QNN_NO_TMA_STORE") != nullptr;   // profiling switch
-  const bool tma_store = !no_tma_store && pl.requant && (pl.out_cs % 16) == 0 &&
+  const bool tma_store = !no_tma_store && !pl.a_rows && pl.requant && (pl.out_cs % 16) == 0 &&
                          (reinterpret_cast<uintptr_t>(output) & 15) == 0;
   if (tma_store) {
     // column groups of one epilogue warp set (gemm_epi_sets): 4 / nsets
@@ -780,6 +834,15 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = pl.g_sw; p.pt = d->pad_t; p.pl = pl.g_pl;
   p.fdQ = make_fastdiv((uint32_t)pl.Q);
   p.fdPQ = make_fastdiv((uint32_t)(pl.P * pl.Q));
+  if (pl.a_rows) {
+    p.a_rows = 1;
+    p.a_Wp = pl.a_Wp;
+    p.a_T = pl.a_T;
+    p.a_nri = pl.a_nri;
+    p.a_stage_bytes = pl.a_stage_bytes;
+    p.fdT = make_fastdiv((uint32_t)pl.a_T);
+    p.fdWp = make_fastdiv((uint32_t)pl.a_Wp);
+  }
   if (pl.a_build) {
     p.a_build = 1;
     p.a_W = d->W; p.a_C = d->C; p.a_S = d->S; p.a_sw = d->stride_w; p.a_pl = d->pad_l;

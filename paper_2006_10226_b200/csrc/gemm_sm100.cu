@@ -49,16 +49,17 @@ constexpr bool kInstrument = false;
 // the pipeline stages carry A only.
 // Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
 // commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes) {
-  const size_t a = (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes,
+                       int a_stage_bytes) {
+  const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
   const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * b : stages * (a + b * kps);
   return 1024 + ring + (size_t)stages * raw_bytes + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
 }
 
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes) {
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes) {
   const size_t budget = 227 * 1024;
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes) > budget) --s;
+  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes) > budget) --s;
   return s;
 }
 
@@ -73,6 +74,38 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* desc, uint64_
 
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
   if (kInstrument && tr && blockIdx.x == 0) tr[slot] = clock64();
+}
+
+// One stage's MMAs from a single thread, kept tight: the descriptors advance by constant
+// strides (no per-MMA index math or parameter reloads), the K=32 steps of a k-block unrolled.
+// Taps (r, s) of an R x S grid: A steps `a_col16` per s and `a_row16` per r, B `b_tap16` per
+// tap (the plain k-block sequence is R = 1, S = nk).  The first MMA overwrites the accumulator
+// unless `acc`.
+template <int KS>
+__device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64_t bd, uint32_t idesc, int R, int S,
+                                             uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16, uint32_t acc) {
+  for (int r = 0; r < R; ++r) {
+    uint64_t ad = ad_row;
+    for (int s = 0; s < S; ++s) {
+#pragma unroll
+      for (int k = 0; k < KS; ++k) umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, k ? 1u : acc);
+      acc = 1;
+      ad += a_col16;
+      bd += b_tap16;
+    }
+    ad_row += a_row16;
+  }
+}
+
+__device__ __forceinline__ void issue_mma(int ksteps, uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, int R,
+                                          int S, uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16,
+                                          uint32_t acc) {
+  if (ksteps == 4)
+    issue_mma_ks<4>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
+  else if (ksteps == 2)
+    issue_mma_ks<2>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
+  else if (ksteps == 1)
+    issue_mma_ks<1>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
 }
 
 template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES>
@@ -94,7 +127,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool b_res = p.b_res;
   const int kps = p.kps;                   // k-blocks per pipeline stage
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)stages * kps * a_bytes;   // ring of B stages, or the resident B (num_kb blocks)
+  const size_t a_stage = p.a_stage_bytes ? (size_t)p.a_stage_bytes : (size_t)kps * a_bytes;   // A bytes / stage
+  uint8_t* sB = smem + (size_t)stages * a_stage;   // ring of B stages, or the resident B (num_kb blocks)
   uint8_t* sRaw = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);   // a_build rows
   uint8_t* sOut = sRaw + (size_t)stages * p.a_raw_bytes;
   const bool tracing = kInstrument && p.trace != nullptr && blockIdx.x == 0;
@@ -180,6 +214,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     const bool skip_a = dbg & 4;
     int m_blk = m_first, n_blk = n_first;
+    if (p.a_rows) {
+      // one box per (tile, channel chunk): input rows p_first - pt .. + a_nri, columns -pl .. + Wp
+      const uint32_t bytes = (uint32_t)(p.a_nri * p.a_Wp * BK);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int n = (int)fdiv((uint32_t)m_blk, p.fdT), tt = m_blk - n * p.a_T;
+        const int p_first = (int)fdiv((uint32_t)(tt * kGemmBM), p.fdWp);
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+          if (tracing && leader && it_p < 256) trace_at(p.trace, 6300 + it_p);
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) {
+            if (tracing && it_p < 2048) trace_at(p.trace, it_p);
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            tma_load_4d(sA + (size_t)stage * a_stage, &tmA, &full[stage], kc * BK, -p.pl, p_first - p.pt, n);
+            if (tracing && it_p < 256) trace_at(p.trace, 6600 + it_p);
+          }
+          __syncwarp();
+          ++it_p;
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        QNN_NEXT_TILE();
+      }
+    }
     if (p.a_build) {
       // raw input rows for the builders: per output row the tile touches, its R filter rows
       // (zero outside the image: TMA OOB fill), one 4-D box each
@@ -203,7 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         QNN_NEXT_TILE();
       }
     }
-    for (int t = p.a_build ? num_tiles : blockIdx.x; t < num_tiles; t += gridDim.x) {   // a_build: done above
+    for (int t = (p.a_build || p.a_rows) ? num_tiles : blockIdx.x; t < num_tiles; t += gridDim.x) {   // done above
       const int m0 = m_blk * kGemmBM;
       int an = 0, ah = 0, aw = 0;
       if (p.im2col) {
@@ -223,7 +282,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (leader) {
           if (tracing && it_p < 2048) trace_at(p.trace, it_p);
           mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * ((b_res ? 0 : b_bytes) + (skip_a ? 0 : a_bytes)));
-          uint8_t* dA = sA + (size_t)(stage * kps) * a_bytes;
+          uint8_t* dA = sA + (size_t)stage * a_stage;
           uint8_t* dB = sB + (size_t)(stage * kps) * b_bytes;
           for (int t2 = 0; t2 < nk; ++t2, dA += a_bytes, dB += b_bytes) {
             const int kb = kb0 + t2;
@@ -287,7 +346,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&empty[stage], phase ^ 1);
       mbar_wait(&rawfull[stage], phase);
       const uint8_t* rp0 = sRaw + (size_t)stage * p.a_raw_bytes + (size_t)(ri - r_first) * p.a_slot_bytes + ab;
-      uint8_t* dA = sA + (size_t)(stage * kps) * a_bytes + (size_t)mi * 32;
+      uint8_t* dA = sA + (size_t)stage * a_stage + (size_t)mi * 32;
       for (int r = r0; r < p.num_kb; r += 2) {
         // 9 aligned words around the window (addresses outside the row only feed masked bytes
         // and stay inside this CTA's shared memory); bytes past S*C are left as they come:
@@ -339,6 +398,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint64_t adesc0 = make_sdesc(smem_u32(sA), BK);
     const uint64_t bdesc0 = make_sdesc(smem_u32(sB), BK);
     const int ksteps = (dbg & 8) ? 0 : BK / 32;
+    // loop-invariant issue parameters in registers (tight issue loops: see issue_mma)
+    const uint32_t idesc = p.idesc;
+    const bool a_rows = p.a_rows;
+    const int nchunks = p.nchunks, num_kb = p.num_kb;
+    const int S_taps = a_rows ? p.S : 1, R_taps = a_rows ? num_kb / (p.S * nchunks) : 1;
+    const uint32_t a_col16 = (uint32_t)BK >> 4, a_row16 = (uint32_t)(p.a_Wp * BK) >> 4;
+    const uint32_t b_tap16 = (uint32_t)(nchunks * b_bytes) >> 4;
     if (b_res) mbar_wait(bres_full, 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int acc = it & (nacc - 1);
@@ -348,20 +414,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (tracing && leader && it < 100) trace_at(p.trace, 7300 + it);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * acc_cols;
-      for (int kb0 = 0; kb0 < p.num_kb; kb0 += kps) {
-        const int nk = min(kps, p.num_kb - kb0);
+      if (a_rows) {
+        // tap (r, s) of channel chunk kc: A starts (r*Wp + s) pixels into the staged input rows
+        const int n = (int)fdiv((uint32_t)t, p.fdT), tt = t - n * p.a_T;   // num_n == 1 (resident B)
+        const int p_first = (int)fdiv((uint32_t)(tt * kGemmBM), p.fdWp);
+        const int off0 = tt * kGemmBM - p_first * p.a_Wp;
+        for (int kc = 0; kc < nchunks; ++kc) {
+          if (tracing && leader && it_m < 256) trace_at(p.trace, 6900 + it_m);
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (leader) {
+            if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
+            const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage) + (uint32_t)(off0 * BK)) >> 4);
+            const uint64_t bd = bdesc0 + (((uint32_t)kc * b_bytes) >> 4);
+            issue_mma(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0);
+            umma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          ++it_m;
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      for (int kb0 = 0; kb0 < (a_rows ? 0 : num_kb); kb0 += kps) {
+        const int nk = min(kps, num_kb - kb0);
         if (tracing && leader && it_m < 256) trace_at(p.trace, 6900 + it_m);
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (leader) {
           if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
-          for (int t = 0; t < nk; ++t) {
-            const int kb = kb0 + t;
-            // descriptors advance by (byte offset >> 4) in the start-address field
-            const uint64_t ad = adesc0 + (((uint32_t)(stage * kps + t) * a_bytes) >> 4);
-            const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb : stage * kps + t) * b_bytes) >> 4);
-            for (int k = 0; k < ksteps; ++k) umma_i8(d_tmem, ad + 2 * k, bd + 2 * k, p.idesc, (kb | k) != 0);
-          }
+          // descriptors advance by (byte offset >> 4) in the start-address field
+          const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage)) >> 4);
+          const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb0 : stage * kps) * b_bytes) >> 4);
+          issue_mma(ksteps, d_tmem, ad, bd, idesc, 1, nk, 0, a_bytes >> 4, b_bytes >> 4, kb0 != 0);
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -466,11 +553,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (t >= num_tiles) break;   // staged for the other sets only
       }
       const int row0 = m_blk * kGemmBM + quad * 32;
-      const int row = row0 + lane;
-      const bool row_ok = row < p.M;
+      int row = row0 + lane;
+      bool row_ok = row < p.M;
       int cls = 0;
       int32_t rterm = 0;
-      if (row_ok) {
+      if (p.a_rows) {
+        // flattened (p, q) with pitch Wp per image: q >= Q (and rows past P) are discarded
+        const int n = (int)fdiv((uint32_t)m_blk, p.fdT), tt = m_blk - n * p.a_T;
+        const int f = tt * kGemmBM + quad * 32 + lane;
+        const int pp = (int)fdiv((uint32_t)f, p.fdWp), qq = f - pp * p.a_Wp;
+        row_ok = qq < p.Q && pp < p.P;
+        row = (n * p.P + pp) * p.Q + qq;
+        if (row_ok) {
+          if (HAS_CLS) cls = (int)e.rowcls[pp] * e.ncc + (int)e.colcls[qq];
+          if (e.rowsum) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
+        }
+      } else if (row_ok) {
         if (HAS_CLS) {
           const int rem = row - (int)fdiv((uint32_t)row, p.fdPQ) * pq;
           const int pp = (int)fdiv((uint32_t)rem, p.fdQ), qq = rem - pp * p.Q;
@@ -528,8 +626,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         *reinterpret_cast<uint4*>(stage_out + ((l16 + 48) ^ sw)) = make_uint4(w[4], w[5], w[6], w[7]);
         if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 3);
       }
+      if (dbg & 32) {   // (instrumented builds) no epilogue work: release the accumulator at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0 && c_begin < c_end) mbar_arrive(&tempty[acc]);
+      }
 #pragma unroll 1
-      for (int j = two ? c_end : c_begin; j < c_end; ++j) {
+      for (int j = two ? c_end : ((dbg & 32) ? c_end : c_begin); j < c_end; ++j) {
         uint32_t v[32];
         if (!(dbg & 16)) tmem_load32(tbase + j * 32, v);
         if (j == c_end - 1) {
@@ -674,7 +777,7 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
     if (dev < 64) attr_done[dev] = 1;
   }
   const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb : 0, p.kps,
-                                      p.a_raw_bytes);
+                                      p.a_raw_bytes, p.a_stage_bytes);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();

@@ -91,6 +91,14 @@ struct GemmParams {
   FastDiv fdP;
   int a_slot_bytes;        // one output row's R raw rows (R * a_rowlen rounded up to 128 B: TMA alignment)
   int a_raw_bytes;         // per-stage raw-row region (a_nr * a_slot_bytes)
+  // a_rows (stride-1 convs with resident weights): per tile and channel chunk ONE tiled TMA box
+  // brings the input rows the tile touches ([a_nri][a_Wp][BK], zero padded) and every tap (r, s)
+  // is an MMA whose A descriptor starts (r*Wp + s) pixels further into it; GEMM rows are the
+  // flattened (p, q) positions with pitch Wp = Q + S - 1 per image (q >= Q rows are discarded)
+  int a_rows;
+  int a_Wp, a_T, a_nri;    // flattened pitch, tiles per image, input rows per box
+  int a_stage_bytes;       // A bytes per pipeline stage (a_rows: a_nri * a_Wp * BK rounded up)
+  FastDiv fdT, fdWp;
   GemmEpilogue e;
 };
 
@@ -117,8 +125,9 @@ __host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles, int nepi =
 }
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
-size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0);
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0);
+size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0,
+                       int a_stage_bytes = 0);
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0, int a_stage_bytes = 0);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 

@@ -303,3 +303,55 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_ABUILD="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+# stride-1 convolutions with resident weights: per (tile, channel chunk) one TMA box of the
+# input rows the tile touches; every tap is an MMA whose A descriptor starts (r*Wp + s) rows in
+AROWS_CASES = [
+    # N, C, H, W, K, R, S, pad(t,l,b,r), a_dtype, w_dtype, zp_W, out
+    (2, 64, 20, 19, 64, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "u8"),      # BK 64 (SW64)
+    (2, 128, 14, 15, 128, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "u8"),    # BK 128 (SW128)
+    (3, 32, 9, 7, 48, 3, 3, (1, 1, 1, 1), "s8", "s8", 0, "s8"),        # BK 32, Wp 9 (many rows per tile)
+    (1, 64, 56, 56, 64, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "u8"),      # ResNet layer1 conv2
+    (2, 64, 11, 9, 64, 3, 3, (1, 1, 1, 1), "u8", "u8", 117, "u8"),     # zp_W != 0 (row sums)
+    (1, 32, 23, 21, 48, 5, 5, (2, 2, 2, 2), "u8", "s8", 0, "u8"),      # 5x5
+    (1, 64, 10, 17, 96, 1, 7, (0, 3, 0, 3), "u8", "s8", 0, "u8"),      # 1x7
+    (1, 64, 17, 10, 96, 7, 1, (3, 0, 3, 0), "u8", "s8", 0, "s8"),      # 7x1
+    (2, 64, 13, 12, 64, 3, 3, (0, 2, 1, 0), "u8", "s8", 0, "u8"),      # asymmetric pad
+    (1, 64, 6, 200, 32, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "u8"),      # wide rows: Wp 202
+    (2, 96, 8, 8, 64, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "s32"),       # raw int32, 3 chunks of 32
+    (2, 256, 7, 7, 256, 3, 3, (1, 1, 1, 1), "u8", "s8", 0, "u8"),      # 2 chunks of 128
+]
+
+
+@pytest.mark.parametrize("cfg", AROWS_CASES, ids=lambda c: f"C{c[1]}_{c[2]}x{c[3]}_k{c[5]}x{c[6]}_{c[11]}")
+@pytest.mark.parametrize("mode", ["upward", "tonearest"])
+def test_stride1_staged_rows_conv(cfg, mode):
+    N, C, H, W, K, R, S, pad, adt, wdt, zpW, odt = cfg
+    case = gen.conv_case(1300 + C + H * 3 + W, N, C, H, W, K, R, S, (1, 1), pad, (1, 1), 1, adt, wdt, zp_W=zpW,
+                         per_channel=zpW == 0, out_dtype=odt, relu=(C % 64 == 0), rounding=mode)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def test_stride1_im2col_path_subprocess():
+    """QNN_NO_AROWS=1 keeps the per-tap TMA im2col path for the same stride-1 shapes."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+for i, (C, H, W) in enumerate([(64, 20, 19), (128, 9, 11)]):
+    case = gen.conv_case(1400 + i, 2, C, H, W, 64, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), 1, "u8", "s8")
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case))
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_AROWS="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])

@@ -49,10 +49,11 @@ def main(rnd="r01"):
     os.makedirs(OUT, exist_ok=True)
     L = load_launches(os.path.join(RUN, "launches.csv"))
     # the last complete step: from the last quantize launch to the following dequantize
-    qidx = [i for i, x in enumerate(L) if "quantize_kernel" in x["name"] and "dequant" not in x["name"]]
+    isq = lambda n: "quantize" in n and "dequantize" not in n and "requantize" not in n
+    qidx = [i for i, x in enumerate(L) if isq(x["name"])]
     step = None
     for qi in reversed(qidx):
-        di = next((j for j in range(qi, len(L)) if "dequantize_kernel" in L[j]["name"]), None)
+        di = next((j for j in range(qi, len(L)) if "dequantize" in L[j]["name"]), None)
         if di is not None:
             step = L[qi:di + 1]
             break
@@ -120,5 +121,47 @@ def main(rnd="r01"):
         json.dump(json.loads(line), open(os.path.join(OUT, f"{rnd}_bench.json"), "w"), indent=1)
 
 
+
+
+def summarize_bw(rnd="r01"):
+    """Depthwise / requantize / quantize / dequantize launches: ncu duration and DRAM bytes,
+    matched in order to the bench_layers rows (algorithmic bytes from the layer shapes)."""
+    import statistics as stt
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6552.3)
+    lines = [f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+             f"dram__throughput.avg.pct_of_peak_sustained_elapsed (cold L2 per launch) of",
+             "`tools/bench_layers.py --suite mobilenet --batch 128` and `--suite requant`;",
+             "GB/s = ALGORITHMIC bytes (bench_layers row) / ncu duration; peak = measured HBM "
+             f"{hbm:.0f} GB/s. DRAM bytes < algorithmic where the output is still in L2 at kernel end.", "",
+             f"{'op':34s} {'kernel':28s} {'us':>8s} {'alg_MB':>8s} {'GB/s':>8s} {'frac':>6s} {'dram_MB':>8s}"]
+    for csvf, logf, pick in (("bw_launches.csv", "bw_plain.log", lambda n: ".dw" in n),
+                             ("rq_launches.csv", "rq_plain.log", lambda n: True)):
+        pc, pl_ = os.path.join(RUN, csvf), os.path.join(RUN, logf)
+        if not (os.path.exists(pc) and os.path.exists(pl_)):
+            continue
+        L = load_launches(pc)
+        groups = []
+        for x in L:
+            key = short(x["name"])
+            if groups and groups[-1][0] == key and len(groups[-1][1]) < 6:
+                groups[-1][1].append(x)
+            else:
+                groups.append((key, [x]))
+        rows = [json.loads(l) for l in open(pl_).read().splitlines() if l.startswith("{")]
+        rows = [r for r in rows if pick(r["name"])]
+        for (key, xs), r in zip(groups, rows):
+            us = stt.median(x.get("gpu__time_duration.sum", 0) for x in xs) / 1e3
+            dram = stt.median(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in xs)
+            alg = r["gbs"] * r["ms"] * 1e6   # bytes
+            gbs = alg / (us * 1e3) if us else 0.0
+            lines.append(f"{r['name']:34s} {key[:28]:28s} {us:8.1f} {alg / 1e6:8.1f} {gbs:8.0f} {gbs / hbm:6.3f} "
+                         f"{dram / 1e6:8.1f}")
+    open(os.path.join(OUT, f"{rnd}_bandwidth_ops_ncu.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 if __name__ == "__main__":
     main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    summarize_bw(sys.argv[1] if len(sys.argv) > 1 else "r01")
