@@ -27,12 +27,24 @@
 // is done by cvt.pack.sat.  Per-column {M, t} and per-(class, column) K are staged
 // once per N-tile in shared memory and read as broadcast LDS.128 (two columns each).
 #include "common.cuh"
+#include <cstdio>
+#include <cstdlib>
+
 #include "epilogue.cuh"
 #include "internal.h"
 
 namespace qnn {
 
-constexpr int kStageOutBytes = kGemmEpiWarps * 4 * 1024;  // per-warp 2 x (32 rows x <= 64 B) output staging
+// per-warp output staging for the TMA store, 32 rows x <= 64 B per buffer.  One buffer: the
+// next tile's writes wait for the previous store to have read it (a few hundred cycles against
+// tile periods of thousands), and the 32 KB saved buys a pipeline stage for the 48-KB-stage
+// GEMMs (BK 128 x BN 256 with border classes: 2 -> 3 stages).  QNN_EPI_STAGE_BUFS=2 restores
+// double buffering.
+#ifndef QNN_EPI_STAGE_BUFS
+#define QNN_EPI_STAGE_BUFS 1
+#endif
+constexpr int kEpiStageBufs = QNN_EPI_STAGE_BUFS;
+constexpr int kStageOutBytes = kGemmEpiWarps * 2048 * kEpiStageBufs;
 constexpr int kParamBytes = 256 * 8 + 256 * 8;            // per-column {M, t} and c
 
 // per-class offset rows in smem: int64 K (UPWARD) or int32 off (TONEAREST / raw), pitch BN + 4
@@ -150,8 +162,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // Warp roles.  The warp scheduler favours higher warp ids, so the latency-critical
   // single-thread roles get the highest ids and are never starved by waiting epilogue warps.
   constexpr int kEpiW = kGemmEpiWarps;        // epilogue warps 0..15
-  constexpr int kProdWarp = kEpiW + 2;        // TMA producer
-  constexpr int kMmaWarp = kEpiW + 3;         // MMA issuer
+  constexpr int kProdWarp = kGemmRoleBase;      // TMA producer
+  constexpr int kMmaWarp = kGemmRoleBase + 1;   // MMA issuer
   constexpr int kAllocWarp = kMmaWarp;        // TMEM allocator (the MMA warp, before its loop)
   if (warp == kProdWarp && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -481,7 +493,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int32_t zp_out = e.zp_out, lo = e.lo, hi = e.hi;
     constexpr bool out8 = MODE != 2;   // requantize => 8-bit output, raw => int32 (abi guarantees it)
     const bool tma_st = e.tma_store;
-    uint8_t* stage_base = sOut + ew * 4096;   // double-buffered across tiles
+    uint8_t* stage_base = sOut + ew * 2048 * kEpiStageBufs;
     int sbuf = 0;
     // staging row pitch = this group's column bytes; swizzle matches the store box (none for 96 B rows)
     const int row_bytes = (c_end - c_begin) * 32;
@@ -583,12 +595,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (tracing && lane == 0 && it < 100) trace_at(p.trace, 9200 + it * 16 + warp);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * acc_cols + ((uint32_t)(quad * 32) << 16);
-      // common case (UPWARD fast path, TMA store, two chunks per warp): both TMEM loads in
-      // flight at once and the accumulator released before any math
+      // common case (UPWARD fast path, TMA store, two chunks per warp, one epilogue set): both
+      // TMEM loads in flight at once and the accumulator released before any math (measured:
+      // a gain at BN 256, a 5-10% loss when several sets share the SM)
 #ifdef QNN_EPI_NO_TWO
       const bool two = false;
 #else
-      const bool two = MODE == 0 && tile_fast && tma_st && !dbg && c_end - c_begin == 2 && !has_res;
+      const bool two = MODE == 0 && nsets == 1 && tile_fast && tma_st && !dbg && c_end - c_begin == 2 && !has_res;
 #endif
       if (two) {
         uint32_t va[32], vb[32];
@@ -601,7 +614,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
-        if (lane == 0) bulk_wait_read<1>();
+        if (lane == 0) bulk_wait_read<kEpiStageBufs - 1>();
         __syncwarp();
         if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 1);
         const long long* kbase = reinterpret_cast<const long long*>(sOff) + cls * offp + c_begin * 32;
@@ -632,7 +645,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0 && c_begin < c_end) mbar_arrive(&tempty[acc]);
       }
 #pragma unroll 1
-      for (int j = two ? c_end : ((dbg & 32) ? c_end : c_begin); j < c_end; ++j) {
+      for (int j = (two || (dbg & 32)) ? c_end : c_begin; j < c_end; ++j) {
         uint32_t v[32];
         if (!(dbg & 16)) tmem_load32(tbase + j * 32, v);
         if (j == c_end - 1) {
@@ -695,7 +708,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (tma_st) {
             if (j == c_begin) {
               // the store issued two tiles ago from this buffer must have finished reading it
-              if (lane == 0) bulk_wait_read<1>();
+              if (lane == 0) bulk_wait_read<kEpiStageBufs - 1>();
               __syncwarp();
             }
             // staged in the TMA swizzle layout of this group's store box
@@ -736,7 +749,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_store_2d(tmC, stage_out, n_blk * BN + c_begin * 32, row0);
           bulk_commit();
         }
-        sbuf ^= 1;
+        if (kEpiStageBufs == 2) sbuf ^= 1;
       }
       if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 4608 + it);
       if (tracing && lane == 0 && it < 100) trace_at(p.trace, 10900 + it * 16 + warp);
@@ -781,7 +794,12 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  static const bool trace_err = std::getenv("QNN_PLAN_TRACE") != nullptr;
+  if (e != cudaSuccess && trace_err)
+    std::fprintf(stderr, "[qnn gemm] launch failed: %s (grid %d, %d threads, %zu B smem)\n", cudaGetErrorString(e),
+                 grid, kGemmThreads, smem);
+  return e;
 }
 
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC, const GemmParams& p,

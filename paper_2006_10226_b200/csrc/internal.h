@@ -104,7 +104,10 @@ struct GemmParams {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmEpiWarps = 16;
-constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;  // + one warpgroup: producer, MMA/allocator, 2 idle
+// 20 warps: the register file is allocated per 4-warp group, so 18 warps would cost as much
+// as 20 (measured: 576 threads x 112 registers does not launch)
+constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;  // + one warpgroup: 2 idle, producer, MMA/allocator
+constexpr int kGemmRoleBase = kGemmEpiWarps + 2;
 
 // TMEM accumulator buffers: 512 columns split into the largest power-of-two count
 // (<= 8) of buffers at least BN wide, so narrow tiles keep more tiles in flight.

@@ -137,6 +137,8 @@ def main():
                 report(f"mbv2_b{b}.{c.name}{'.dw' if c.groups > 1 else ''}", t.time(fn, args.reps), macs, by)
         elif suite == "dense":
             for n in (512, 1024, 2048, 4096, 8192):
+                if args.only and args.only != f"dense_{n}":
+                    continue
                 case = gen.dense_case(3000 + n, n, n, n)
                 dev = torch.device("cuda")
                 op = qnn.PackedDense(n, torch.from_numpy(case.W).to(dev), torch.from_numpy(case.bias).to(dev),
