@@ -186,6 +186,7 @@ struct ConvPlan {
   // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
   int gW = 0, gS = 0, g_sw = 0, g_pl = 0, g_pr = 0, g_dw = 0;
   int BK = 0, nchunks = 0, Cw = 0, BN = 0, Kpad = 0, num_n = 0, num_m = 0, stages = 0, b_res_kb = 0, kps = 1;
+  int grid = 0;   // persistent CTAs (a multiple of num_n when tiles > SMs)
   bool im2col = false;
   ClassTable ct{};
   std::vector<uint8_t> rowcls, colcls;
@@ -370,22 +371,33 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   pl.num_m = (int)((pl.M + kGemmBM - 1) / kGemmBM);
   {
     // N tiling: fewest N tiles (BN <= 256) unless narrower tiles fill the persistent grid's last
-    // round better -- cost ~ rounds x (BN + 32), rounds = ceil(tiles / SMs) (wave quantisation of
-    // the small-M deep layers, e.g. ResNet-50 layer4 at batch 256: 196 tiles on 148 SMs)
+    // round better -- cost ~ rounds x (BN + 32) (wave quantisation of the small-M deep layers,
+    // e.g. ResNet-50 layer4 at batch 256: 196 tiles on 148 SMs).  With several N tiles and more
+    // tiles than SMs the grid is a multiple of num_n, so every CTA keeps one N tile (tile t =
+    // m * num_n + n, t += grid): its per-column epilogue parameters are staged once and its
+    // weights can stay resident; rounds = ceil(num_m / (grid / num_n)).
     const int sms = sm_count();
+    // QNN_NO_NSTAT=1: the plain persistent order (A/B measurements)
+    static const bool no_nstat = std::getenv("QNN_NO_NSTAT") != nullptr;
     const int n0 = (d->K + 255) / 256;
     long long best = -1;
     for (int nn = n0; nn <= std::max(n0, (d->K + 63) / 64); ++nn) {
       const int bn = round_up((d->K + nn - 1) / nn, 32);
       if (bn < 64 && nn > n0) break;
+      if (nn > sms) break;
       const long long tiles = (long long)pl.num_m * nn;
-      const long long cost = (tiles + sms - 1) / sms * (bn + 32);
+      const long long rounds = tiles <= sms ? 1
+                               : no_nstat ? (tiles + sms - 1) / sms
+                                          : (pl.num_m + sms / nn - 1) / (sms / nn);
+      const long long cost = rounds * (bn + 32);
       if (best < 0 || cost < best) {
         best = cost;
         pl.num_n = nn;
         pl.BN = bn;
       }
     }
+    const long long tiles = (long long)pl.num_m * pl.num_n;
+    pl.grid = tiles <= sms ? (int)tiles : no_nstat ? sms : (sms / pl.num_n) * pl.num_n;
   }
   pl.Kpad = pl.num_n * pl.BN;
   pl.im2col = !(d->R == 1 && pl.gS == 1 && d->stride_h == 1 && pl.g_sw == 1 && d->pad_t == 0 && pl.g_pl == 0 &&
@@ -407,7 +419,9 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     const int num_kb = d->R * pl.gS * pl.nchunks;
     // keep the whole weight operand resident when it is one N tile and leaves room for >= 4 A stages
     pl.b_res_kb = 0;
-    if (pl.num_n == 1 && gemm_smem_bytes(pl.BK, pl.BN, 4, ncls, num_kb, 1) <= 227 * 1024) pl.b_res_kb = num_kb;
+    // (several N tiles: each CTA keeps one, see the grid above)
+    const bool one_n = pl.num_n == 1 || pl.grid % pl.num_n == 0;
+    if (one_n && gemm_smem_bytes(pl.BK, pl.BN, 4, ncls, num_kb, 1) <= 227 * 1024) pl.b_res_kb = num_kb;
     // k-blocks per stage: about 32 KB of operands per barrier round trip, at least 3 stages
     const int per_kb = kGemmBM * pl.BK + (pl.b_res_kb ? 0 : pl.BN * pl.BK);
     pl.kps = std::max(1, std::min(num_kb, 32768 / per_kb));
@@ -422,7 +436,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   static const bool no_abuild = std::getenv("QNN_NO_ABUILD") != nullptr;
   {
     const long long rowlen = (long long)d->W * d->C;
-    pl.a_build = !no_abuild && pl.fold && pl.BK == 32 && pl.nchunks == 1 && pl.b_res_kb > 0 &&
+    pl.a_build = !no_abuild && pl.num_n == 1 && pl.fold && pl.BK == 32 && pl.nchunks == 1 && pl.b_res_kb > 0 &&
                  d->S * d->C <= 32 && pl.in_cs == d->C && d->dil_w == 1 && rowlen % 16 == 0 &&
                  (long long)(d->R - 1) * d->dil_h + 1 <= 256;
     if (pl.a_build) {
@@ -486,6 +500,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
         pl.kps = d->R * d->S;
         pl.stages = st;
         pl.num_m = d->N * T;
+        pl.grid = std::min(pl.num_m, sm_count());   // num_n == 1
       }
     }
   }
@@ -884,8 +899,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     ep.res_zp = res->zp;
     ep.res_s8 = res->dtype == QNN_S8;
   }
-  const int tiles = pl.num_m * pl.num_n;
-  const int grid = std::min(tiles, sm_count());
+  const int grid = pl.grid;
   int64_t qlo = INT32_MIN, qhi = INT32_MAX;
   if (pl.requant) dtype_range(pl.out_dt, &qlo, &qhi);
   // the residual can push the sum past [lo, hi] even when those are the dtype bounds, but

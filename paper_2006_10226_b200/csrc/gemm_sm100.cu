@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // weights are shared by every tile of this CTA: load them once
       if (leader) {
         mbar_arrive_expect_tx(bres_full, (uint32_t)p.num_kb * b_bytes);
-        for (int kb = 0; kb < p.num_kb; ++kb) tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, 0);
+        // (a CTA keeps one N tile for all its tiles: grid % num_n == 0, see the host plan)
+        for (int kb = 0; kb < p.num_kb; ++kb)
+          tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, n_first * BN);
       }
       __syncwarp();
     }
