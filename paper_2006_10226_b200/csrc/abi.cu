@@ -649,11 +649,13 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   const int a_signed = d->input_dtype == QNN_S8;
 
   if (pl.depthwise) {
-    // kernel choice: 3x3 dp4a (CUDA cores) > tensor-core path > generic CUDA-core kernel.
-    // QNN_DW_IMPL=tc|generic forces one of the others (A/B measurements).
+    // kernel choice: 3x3 TMA-staged (CUDA cores) > 3x3 register-blocked dp4a > tensor-core
+    // path > generic CUDA-core kernel.  QNN_DW_IMPL=dp4a|tc|generic forces one of the others
+    // (A/B measurements).
     static const char* dw_impl = std::getenv("QNN_DW_IMPL");
     const bool force_tc = dw_impl && std::strcmp(dw_impl, "tc") == 0;
     const bool force_generic = dw_impl && std::strcmp(dw_impl, "generic") == 0;
+    const bool force_dp4a = dw_impl && std::strcmp(dw_impl, "dp4a") == 0;
     const bool no_dwtc = force_generic;
     DwParams p{};
     p.in = input;
@@ -681,6 +683,23 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
       int64_t qlo, qhi;
       dtype_range(pl.out_dt == DT_S8 ? QNN_S8 : (pl.out_dt == DT_U8 ? QNN_U8 : QNN_S32), &qlo, &qhi);
       const int clamp = pl.lo > qlo ? 2 : (pl.hi < qhi ? 1 : 0);   // the saturating pack covers the dtype range
+      DwParams pt = p;
+      if (!force_dp4a && dwtma_plan(pt) && load_driver_entry_points()) {
+        // input (c, w, h, n); box = CS channels x Wb columns x band rows, zero outside the image
+        alignas(64) CUtensorMap tm;
+        const cuuint64_t dims[4] = {(cuuint64_t)d->C, (cuuint64_t)d->W, (cuuint64_t)d->H, (cuuint64_t)d->N};
+        const cuuint64_t strides[3] = {(cuuint64_t)pl.in_cs, (cuuint64_t)pl.in_cs * d->W,
+                                       (cuuint64_t)pl.in_cs * d->W * d->H};
+        const cuuint32_t box[4] = {(cuuint32_t)pt.dwt_cs, (cuuint32_t)pt.dwt_wb,
+                                   (cuuint32_t)((pt.dwt_bp - 1) * pt.sh + 3), 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (p_encode_tiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(input), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+          small_tensor_fixup(&tm, (uint64_t)pl.in_cs * d->W * d->H * d->N);
+          return cuda_status(launch_depthwise_tma(tm, pt, clamp, s));
+        }
+      }
       if (launch_depthwise3(p, clamp, s)) return cuda_status(cudaGetLastError());
     }
     if (pl.dwtc && !no_dwtc && pl.requant && (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) &&

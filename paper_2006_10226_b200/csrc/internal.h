@@ -177,9 +177,13 @@ struct DwParams {
   int32_t zp_out, lo, hi;
   int w_fits_s8;           // every W - zp_W in [-128, 127] (dp4a path)
   int qseg;                // dp4a path: column blocks per task (set by the launcher)
+  int dwt_cs, dwt_wb, dwt_bp, dwt_stage_bytes;   // TMA-staged path: channel slice, box width, rows/band
 };
 cudaError_t launch_depthwise(const DwParams& p, cudaStream_t s);
 bool launch_depthwise3(const DwParams& p, int clamp, cudaStream_t s);   // clamp: 0 none, 1 hi, 2 lo+hi
+// 3x3 depthwise with TMA-staged input bands (depthwise_tma.cu): plan fills the dwt_* fields
+bool dwtma_plan(DwParams& p);
+cudaError_t launch_depthwise_tma(const CUtensorMap& tm, const DwParams& p, int clamp, cudaStream_t s);
 
 // Tensor-core depthwise conv (depthwise_tc.cu): C % 16 == 0, s8 weights with zp_W == 0,
 // stride 1 or 2, 8-bit requantized output.

@@ -226,8 +226,9 @@ def test_depthwise_tensor_core_path(cfg):
 
 
 def test_depthwise_forced_kernels_subprocess():
-    """The 3x3 shapes normally take the dp4a kernel; run the tensor-core and the generic
-    kernels on them too (QNN_DW_IMPL is read once per process, hence the subprocess)."""
+    """The 3x3 shapes normally take the TMA-staged kernel; run the register-blocked dp4a, the
+    tensor-core and the generic kernels on them too (QNN_DW_IMPL is read once per process,
+    hence the subprocess)."""
     import os
     import subprocess
     import sys
@@ -245,7 +246,7 @@ for cfg in [(2, 32, 30, 37, 1, "upward"), (3, 96, 14, 14, 2, "tonearest"), (1, 4
 print("OK")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for impl in ("tc", "generic"):
+    for impl in ("dp4a", "tc", "generic"):
         env = dict(os.environ, QNN_DW_IMPL=impl)
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                            timeout=600)
@@ -303,6 +304,30 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_ABUILD="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+# TMA-staged 3x3 depthwise: channel slices (CS 16/32/64), multi-band images, odd widths, pad
+# variants, zp_W != 0 (weights W - zp_W still in s8), s8 activations, last partial bands
+DWT_CASES = [
+    # N, C, H, W, stride, pad, a_dtype, w_dtype, zp_W, out, rounding
+    (2, 32, 40, 37, 1, (1, 1, 1, 1), "u8", "s8", 0, "u8", "upward"),
+    (2, 144, 19, 21, 1, (1, 1, 1, 1), "u8", "s8", 0, "u8", "upward"),     # CS 16
+    (1, 192, 29, 23, 2, (1, 1, 1, 1), "u8", "s8", 0, "u8", "upward"),     # CS 64, stride 2, odd
+    (3, 96, 17, 17, 2, (0, 0, 1, 1), "s8", "s8", 0, "s8", "upward"),      # asymmetric pad
+    (2, 64, 13, 9, 1, (0, 0, 0, 0), "u8", "u8", 121, "u8", "upward"),     # no pad, zp_W
+    (1, 48, 33, 30, 1, (1, 1, 1, 1), "u8", "s8", 0, "u8", "tonearest"),   # generic rounding path
+    (1, 32, 112, 112, 1, (1, 1, 1, 1), "u8", "s8", 0, "u8", "upward"),    # MobileNet block0 shape
+]
+
+
+@pytest.mark.parametrize("cfg", DWT_CASES, ids=lambda c: f"C{c[1]}_{c[2]}x{c[3]}_s{c[4]}_{c[10]}")
+def test_depthwise_tma_staged(cfg):
+    N, C, H, W, st, pad, adt, wdt, zpW, odt, mode = cfg
+    case = gen.conv_case(1500 + C + H, N, C, H, W, C, 3, 3, (st, st), pad, (1, 1), C, adt, wdt, zp_W=zpW,
+                         per_channel=zpW == 0, out_dtype=odt, relu=True, act6=(C % 64 == 0), rounding=mode)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
 
 
 # stride-1 convolutions with resident weights: per (tile, channel chunk) one TMA box of the
