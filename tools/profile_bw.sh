@@ -1,0 +1,6 @@
+OUT=gpurun_out
+python tools/bench_layers.py --suite mobilenet --batch 128 --reps 3 > $OUT/bw_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
+  -k regex:"dw3_tma|depthwise|requantize|quantize|dequantize" --csv --log-file $OUT/bw_launches.csv \
+  python tools/bench_layers.py --suite mobilenet --batch 128 --reps 3 > $OUT/ncu_bw.log 2>&1
+echo "bw rc=$?"
