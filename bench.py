@@ -639,7 +639,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "note": "pinned f32 images H2D (copy stream, double-buffered: step k+1's copy overlaps step k) + graph + f32 logits D2H, every step"},
         "gpu_launches": int(net.launches_per_step * args.steps),
-        "roofline": {"kernel": "qnn_gemm_i8_kernel (all 54 conv/fc launches of a step)", "bound": "tensor",
+        "roofline": {"kernel": "tcgen05 GEMMs: qnn_gemm_i8_kernel + qnn_gemm_t_kernel (all 54 conv/fc launches of a step)", "bound": "tensor",
                      "achieved": round(achieved, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
                      "frac": round(achieved / int8_peak, 4),
                      "peak_note": "int8 dense = 2 x measured sustained bf16 (MEASURED_PEAKS.json) per the guide's "

@@ -778,6 +778,51 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     }
   }
 
+  // wide pointwise layers: the channel-major GEMM (gemm_t.cu) keeps each output channel's
+  // requantize constants in its TMEM lane's registers.  QNN_NO_TRANS=1 keeps the pixel-major
+  // kernel (A/B measurements).
+  static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
+  if (!no_trans && !res && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
+      d->groups == 1 && d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
+      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && d->K % 128 == 0 && d->K >= 256 && pl.out_cs % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(output) & 15) == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
+    const int num_kb = pl.nchunks;   // one tap
+    const int stages = gemm_t_max_stages(pl.BK, num_kb);
+    if (stages >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, stages) <= 226 * 1024) {
+      alignas(64) CUtensorMap tmX, tmW, tmC;
+      const int a_chan = d->C;
+      bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, 256) &&
+                 encode_2d(&tmW, pk + pl.pk_w, (uint64_t)pl.Cw, (uint64_t)pl.Kpad, (uint64_t)pl.Cw, pl.BK, 128) &&
+                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 64, false);
+      if (okt) {
+        GemmTParams tp{};
+        tp.BK = pl.BK;
+        tp.stages = stages;
+        tp.num_kb = num_kb;
+        tp.num_ch_tiles = d->K / 128;
+        tp.num_px_tiles = (int)((pl.M + 255) / 256);
+        tp.idesc = make_idesc_i8(1, a_signed, 128, 256);   // A = s8 weights, B = activations
+        tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
+        tp.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
+        tp.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
+        tp.zp_out = pl.zp_out;
+        tp.lo = pl.lo;
+        tp.hi = pl.hi;
+        {
+          static const char* dbg_env = std::getenv("QNN_GEMM_DEBUG");
+          tp.dbg = dbg_env ? std::atoi(dbg_env) : 0;
+        }
+        const int sms = sm_count();
+        const int tiles = tp.num_ch_tiles * tp.num_px_tiles;
+        const int grid = tiles <= sms ? tiles : std::max(1, sms / tp.num_ch_tiles) * tp.num_ch_tiles;
+        int64_t qlo, qhi;
+        dtype_range(pl.out_dt == DT_S8 ? QNN_S8 : QNN_U8, &qlo, &qhi);
+        const bool clamp = pl.lo > qlo || pl.hi < qhi;
+        return cuda_status(launch_gemm_t(tmX, tmW, tmC, tp, pl.mode, clamp, pl.out_dt == DT_S8, grid, s));
+      }
+    }
+  }
+
   alignas(64) CUtensorMap tmA, tmB;
   bool ok;
   const int a_chan = (pl.pad_copy || pl.fold) ? pl.Ct : d->C;

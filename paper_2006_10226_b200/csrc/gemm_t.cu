@@ -1,0 +1,279 @@
+// gemm_t.cu — channel-major ("transposed") tcgen05 GEMM for wide pointwise convolutions
+// (SURVEY §8 rows a3 + a4: the Term-1 contraction and the fused requantize of Eq. 5,
+// P:273-281, for 1x1 / stride-1 / unpadded qnn.conv2d with K_out % 128 == 0, zp_W == 0).
+//
+// The pixel-major kernel (gemm_sm100.cu) puts output pixels on the TMEM lanes, so every
+// epilogue lane needs every column's requantize constants: one shared-memory broadcast per
+// (lane-row, column pair), and the wide 1x1 layers (K_out 256..2048 over a short reduction)
+// are bound by that epilogue.  Here the MMA computes D^T = W * A^T: M = 128 output channels
+// (A operand = the packed weights, resident in shared memory for the CTA's channel block),
+// N = 256 pixels (B operand = the activation rows, streamed by TMA), so a TMEM lane is ONE
+// output channel and its multiplier / shift / 64-bit constant live in that lane's registers
+// for the whole kernel.  Bytes go to a [64 pixels][32 channels] staging tile with one STS.U8
+// each and leave by TMA store.
+//
+// Grid: a multiple of the channel-block count, so a CTA keeps one channel block (weights and
+// constants loaded once); pixel tiles advance by grid / blocks.
+// Warps: 0-15 epilogue (warp w: TMEM lanes 32*(w%4) = its 32 channels, pixel columns
+// 64*(w/4)), 16 TMA producer, 17 MMA issuer + TMEM allocator (2 accumulators x 256 columns).
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "epilogue.cuh"
+#include "internal.h"
+
+namespace qnn {
+
+namespace {
+
+constexpr int kTEpiWarps = 16;
+constexpr int kTThreads = 32 * kTEpiWarps + 64;
+constexpr int kTBM = 128;   // output channels per tile (MMA M)
+constexpr int kTBN = 256;   // pixels per tile (MMA N)
+constexpr int kTStageOut = 2048;   // per epilogue warp: 64 pixels x 32 channels
+
+__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+// two outputs of one channel (pixels j, j+1): clamp, saturate, one byte each into the
+// [pixel][channel] staging tile
+template <bool CLAMP, bool S8OUT>
+__device__ __forceinline__ void store2(uint32_t a, int32_t y0, int32_t y1, int32_t lo, int32_t hi) {
+  if (CLAMP) {
+    y0 = min(max(y0, lo), hi);
+    y1 = min(max(y1, lo), hi);
+  }
+  uint32_t b2;   // saturated bytes (y0, y1) in the low half-word
+  if (S8OUT)
+    asm("cvt.pack.sat.s8.s32.b32 %0, %2, %1, 0;" : "=r"(b2) : "r"(y0), "r"(y1));
+  else
+    asm("cvt.pack.sat.u8.s32.b32 %0, %2, %1, 0;" : "=r"(b2) : "r"(y0), "r"(y1));
+  sts_u8(a, b2);
+  sts_u8(a + 32, b2 >> 8);
+}
+
+// hi32(v * M + K) (64-bit addend): one IMAD.WIDE
+__device__ __forceinline__ int32_t madwide_hi(int32_t v, int32_t M, long long K) {
+  long long d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(v), "r"(M), "l"(K));
+  return (int32_t)((unsigned long long)d >> 32);
+}
+
+}  // namespace
+
+constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers are static)
+
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages) {
+  return 1024 + (size_t)stages * kTBN * BK + (size_t)num_kb * kTBM * BK + (size_t)kTEpiWarps * kTStageOut + 256;
+}
+
+int gemm_t_max_stages(int BK, int num_kb) {
+  int s = 6;
+  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s) > (size_t)kTSmemMax) --s;
+  return s;
+}
+
+template <int MODE, bool CLAMP, bool S8OUT>
+__global__ void __launch_bounds__(kTThreads, 1)
+    qnn_gemm_t_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmTParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int BK = p.BK, stages = p.stages, num_kb = p.num_kb;
+  const uint32_t x_bytes = (uint32_t)kTBN * BK, w_bytes = (uint32_t)kTBM * BK;
+  uint8_t* sX = smem;                                  // stages x [256 pixels][BK]
+  uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb x [128 channels][BK], resident
+  uint8_t* sOut = sW + (size_t)num_kb * w_bytes;       // 16 x [64 pixels][32 channels]
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2], wfull;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kProdWarp = kTEpiWarps, kMmaWarp = kTEpiWarps + 1;
+  const int nct = p.num_ch_tiles, npt = p.num_px_tiles;
+  const int ch = blockIdx.x % nct;                  // fixed channel block (gridDim.x % nct == 0)
+  const int px_first = blockIdx.x / nct, px_step = gridDim.x / nct;
+  if (warp == kProdWarp && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kTEpiWarps);
+    }
+    mbar_init(&wfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc(&tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  if (warp == kProdWarp) {
+    const bool leader = elect_one();
+    if (leader && px_first < npt) {
+      mbar_arrive_expect_tx(&wfull, (uint32_t)num_kb * w_bytes);
+      for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int pt = px_first; pt < npt; pt += px_step) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) {
+          mbar_arrive_expect_tx(&full[stage], x_bytes);
+          tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
+        }
+        __syncwarp();
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    const bool leader = elect_one();
+    const uint64_t wdesc0 = make_sdesc(smem_u32(sW), BK), xdesc0 = make_sdesc(smem_u32(sX), BK);
+    const uint32_t idesc = p.idesc, w16 = w_bytes >> 4, x16 = x_bytes >> 4;
+    const int ksteps = BK / 32;
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    if (px_first < npt) mbar_wait(&wfull, 0);
+    for (int pt = px_first; pt < npt; pt += px_step, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)acc * kTBN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (leader) {
+          const uint64_t wd = wdesc0 + (uint64_t)kb * w16, xd = xdesc0 + (uint64_t)stage * x16;
+          for (int k = 0; k < ksteps; ++k) umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (leader) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp < kTEpiWarps) {
+    // ---------------------------------------------------------------- epilogue
+    const int quad = warp & 3, grp = warp >> 2;
+    const int k = ch * kTBM + quad * 32 + lane;   // this lane's output channel
+    const int32_t M = p.mult[k], rsh = p.rsh[k];
+    const long long off = p.off64[k];
+    const bool fast = MODE == 0 && rsh >= 33 && rsh <= 52;
+    int t = 0;
+    long long K = 0;
+    if (fast) {
+      t = rsh - 32;
+      const unsigned long long c64 = (1ull << (t - 1)) + ((unsigned long long)(long long)p.zp_out << t);
+      K = (long long)((unsigned long long)off * (unsigned long long)(long long)M + (c64 << 32));
+    }
+    const bool all_fast = __all_sync(0xffffffffu, fast);
+    uint8_t* stage_out = sOut + warp * kTStageOut;
+    const uint32_t st_lane = smem_u32(stage_out) + (uint32_t)lane;
+    int it = 0;
+    for (int pt = px_first; pt < npt; pt += px_step, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 64);
+      uint32_t va[32], vb[32];
+      tmem_ld32_nowait(tb, va);
+      tmem_ld32_nowait(tb + 32, vb);
+      tmem_wait32(va);
+      tmem_wait32(vb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&tempty[acc]);
+        bulk_wait_read<0>();   // the previous tile's store has read the staging tile
+      }
+      __syncwarp();
+      // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
+      if (p.dbg & 1) {
+      } else if (all_fast) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* v = h ? vb : va;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            store2<CLAMP, S8OUT>(st_lane + (uint32_t)((h * 32 + j) * 32), madwide_hi((int32_t)v[j], M, K) >> t,
+                                 madwide_hi((int32_t)v[j + 1], M, K) >> t, p.lo, p.hi);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* v = h ? vb : va;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            int32_t y0, y1;
+            if (fast) {
+              y0 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j] * M) + (unsigned long long)K) >> 32) >> t;
+              y1 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j + 1] * M) + (unsigned long long)K) >> 32) >>
+                   t;
+            } else {
+              y0 = rq_apply((long long)(int32_t)v[j] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
+              y1 = rq_apply((long long)(int32_t)v[j + 1] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
+            }
+            store2<CLAMP, S8OUT>(st_lane + (uint32_t)((h * 32 + j) * 32), y0, y1, p.lo, p.hi);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && !(p.dbg & 2)) {
+        tma_store_2d(&tmC, stage_out, ch * kTBM + quad * 32, pt * kTBN + grp * 64);
+        bulk_commit();
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
+                          const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream) {
+  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages);
+  if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
+#define QNN_GT(M_, C_, S_)                                                                                 \
+  if (mode == M_ && clamp == C_ && s8out == S_) {                                                          \
+    auto kern = qnn_gemm_t_kernel<M_, C_, S_>;                                                             \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmemMax);  \
+      if (e != cudaSuccess) return e;                                                                      \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    kern<<<grid, kTThreads, smem, stream>>>(tmX, tmW, tmC, p);                                             \
+    count_launch();                                                                                        \
+    const cudaError_t e = cudaGetLastError();                                                              \
+    if (e != cudaSuccess && std::getenv("QNN_PLAN_TRACE"))                                                 \
+      std::fprintf(stderr, "[qnn gemm_t] launch failed: %s\n", cudaGetErrorString(e));                    \
+    return e;                                                                                              \
+  }
+  QNN_GT(0, false, false) QNN_GT(0, false, true) QNN_GT(0, true, false) QNN_GT(0, true, true)
+  QNN_GT(1, false, false) QNN_GT(1, false, true) QNN_GT(1, true, false) QNN_GT(1, true, true)
+#undef QNN_GT
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace qnn

@@ -62,6 +62,22 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
 }
 #endif
 
+// Channel-major GEMM (gemm_t.cu): wide 1x1 convs, D^T = W * A^T with the output channels on
+// the TMEM lanes (per-lane requantize constants in registers).
+struct GemmTParams {
+  int BK, stages, num_kb, num_ch_tiles, num_px_tiles;
+  uint32_t idesc;
+  const int32_t* mult;   // [Kpad]
+  const int32_t* rsh;    // [Kpad]
+  const int64_t* off64;  // [Kpad] (single border class)
+  int32_t zp_out, lo, hi;
+  int dbg;   // QNN_GEMM_DEBUG (profiling): 1 skips the epilogue math, 2 the TMA stores
+};
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages);
+int gemm_t_max_stages(int BK, int num_kb);
+cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
+                          const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream);
+
 struct GemmParams {
   int M, Nout;
   int num_kb, nchunks, S, dil_h, dil_w;

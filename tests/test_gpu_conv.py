@@ -380,3 +380,49 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_AROWS="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+# wide pointwise convs on the channel-major GEMM (gemm_t.cu): output channels on the TMEM
+# lanes; ragged pixel tails, 1..4 k-blocks, every BK, s8 in/out, clamps, TONEAREST (generic)
+TRANS_CASES = [
+    # N, C, H, W, K, a_dtype, out, relu, act6, rounding
+    (2, 64, 9, 9, 256, "u8", "u8", True, False, "upward"),
+    (1, 128, 28, 28, 512, "u8", "u8", True, False, "upward"),
+    (2, 256, 14, 14, 1024, "s8", "s8", False, False, "upward"),
+    (1, 512, 7, 7, 2048, "u8", "u8", True, False, "upward"),
+    (3, 96, 5, 7, 384, "u8", "u8", True, True, "upward"),       # BK 32 x 3 chunks, clamp
+    (2, 64, 6, 11, 256, "u8", "u8", True, False, "tonearest"),  # per-lane generic rounding
+    (1, 640, 4, 4, 256, "u8", "s8", False, False, "upward"),    # 5 k-blocks of 128
+]
+
+
+@pytest.mark.parametrize("cfg", TRANS_CASES, ids=lambda c: f"C{c[1]}_K{c[4]}_{c[2]}x{c[3]}_{c[9]}")
+def test_wide_pointwise_channel_major(cfg):
+    N, C, H, W, K, adt, odt, relu, act6, mode = cfg
+    case = gen.conv_case(1600 + C + K, N, C, H, W, K, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), 1, adt, "s8",
+                         out_dtype=odt, relu=relu, act6=act6, rounding=mode)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def test_wide_pointwise_pixel_major_subprocess():
+    """QNN_NO_TRANS=1 keeps the pixel-major kernel for the same shapes."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+for i, (C, K) in enumerate([(64, 256), (256, 512)]):
+    case = gen.conv_case(1700 + i, 2, C, 9, 10, K, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), 1, "u8", "s8")
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case))
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_TRANS="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
