@@ -116,6 +116,7 @@ struct GemmParams {
   int a_stage_bytes;       // A bytes per pipeline stage (a_rows: a_nri * a_Wp * BK rounded up)
   FastDiv fdT, fdWp;
   GemmEpilogue e;
+  int mma2;   // two MMA-issuing warps taking alternate tiles (narrow tiles)
 };
 
 constexpr int kGemmBM = 128;

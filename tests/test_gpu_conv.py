@@ -426,3 +426,28 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_NO_TRANS="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+def test_two_mma_issuers_subprocess():
+    """QNN_MMA2=1: two MMA-issuing warps on alternate tiles, each with half of the stage ring
+    (stride-1 staged rows, im2col with streamed weights, 1x1 with resident weights)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+cfgs = [(4, 64, 20, 19, 64, 3, 3, (1, 1), (1, 1, 1, 1)), (3, 128, 17, 15, 128, 3, 3, (2, 2), (1, 1, 1, 1)),
+        (4, 256, 14, 13, 64, 1, 1, (1, 1), (0, 0, 0, 0))]
+for i, (N, C, H, W, K, R, S, st, pad) in enumerate(cfgs):
+    case = gen.conv_case(1800 + i, N, C, H, W, K, R, S, st, pad, (1, 1), 1, "u8", "s8")
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case)), i
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_MMA2="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
