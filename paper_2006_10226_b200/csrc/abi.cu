@@ -787,8 +787,10 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
       (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && d->K % 128 == 0 && d->K >= 256 && pl.out_cs % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(output) & 15) == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
     const int num_kb = pl.nchunks;   // one tap
-    const int stages = gemm_t_max_stages(pl.BK, num_kb);
-    if (stages >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, stages) <= 226 * 1024) {
+    bool w_res = gemm_t_max_stages(pl.BK, num_kb, true) >= 3 &&
+                 gemm_t_smem_bytes(pl.BK, num_kb, gemm_t_max_stages(pl.BK, num_kb, true), true) <= 226 * 1024;
+    const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res);
+    if (stages >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res) <= 226 * 1024) {
       alignas(64) CUtensorMap tmX, tmW, tmC;
       const int a_chan = d->C;
       bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, 256) &&
@@ -799,6 +801,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         tp.BK = pl.BK;
         tp.stages = stages;
         tp.num_kb = num_kb;
+        tp.w_res = w_res;
         tp.num_ch_tiles = d->K / 128;
         tp.num_px_tiles = (int)((pl.M + 255) / 256);
         tp.idesc = make_idesc_i8(1, a_signed, 128, 256);   // A = s8 weights, B = activations

@@ -13,7 +13,8 @@
 // each and leave by TMA store.
 //
 // Grid: a multiple of the channel-block count, so a CTA keeps one channel block (weights and
-// constants loaded once); pixel tiles advance by grid / blocks.
+// constants loaded once; weights streamed per stage when the block does not fit); pixel
+// tiles advance by grid / blocks.
 // Warps: 0-15 epilogue (warp w: TMEM lanes 32*(w%4) = its 32 channels, pixel columns
 // 64*(w/4)), 16 TMA producer, 17 MMA issuer + TMEM allocator (2 accumulators x 256 columns).
 #include <cstdint>
@@ -65,13 +66,17 @@ __device__ __forceinline__ int32_t madwide_hi(int32_t v, int32_t M, long long K)
 
 constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers are static)
 
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages) {
-  return 1024 + (size_t)stages * kTBN * BK + (size_t)num_kb * kTBM * BK + (size_t)kTEpiWarps * kTStageOut + 256;
+// w_res: the CTA's weight block stays resident (num_kb blocks); otherwise each pipeline stage
+// carries its weight k-block next to the activation k-block
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res) {
+  const size_t stage = (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK);
+  return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK : 0) +
+         (size_t)kTEpiWarps * kTStageOut + 256;
 }
 
-int gemm_t_max_stages(int BK, int num_kb) {
+int gemm_t_max_stages(int BK, int num_kb, bool w_res) {
   int s = 6;
-  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s) > (size_t)kTSmemMax) --s;
+  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s, w_res) > (size_t)kTSmemMax) --s;
   return s;
 }
 
@@ -83,9 +88,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int BK = p.BK, stages = p.stages, num_kb = p.num_kb;
   const uint32_t x_bytes = (uint32_t)kTBN * BK, w_bytes = (uint32_t)kTBM * BK;
+  const bool w_res = p.w_res;
   uint8_t* sX = smem;                                  // stages x [256 pixels][BK]
-  uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb x [128 channels][BK], resident
-  uint8_t* sOut = sW + (size_t)num_kb * w_bytes;       // 16 x [64 pixels][32 channels]
+  uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb (resident) or stages x [128 channels][BK]
+  uint8_t* sOut = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // 16 x [64 pixels][32 channels]
   __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2], wfull;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 
   if (warp == kProdWarp) {
     const bool leader = elect_one();
-    if (leader && px_first < npt) {
+    if (leader && w_res && px_first < npt) {
       mbar_arrive_expect_tx(&wfull, (uint32_t)num_kb * w_bytes);
       for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
     }
@@ -126,8 +132,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
-          mbar_arrive_expect_tx(&full[stage], x_bytes);
+          mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes));
           tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
+          if (!w_res) tma_load_2d(sW + (size_t)stage * w_bytes, &tmW, &full[stage], kb * BK, ch * kTBM);
         }
         __syncwarp();
         if (++stage == stages) {
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const int ksteps = BK / 32;
     int stage = 0, it = 0;
     uint32_t phase = 0;
-    if (px_first < npt) mbar_wait(&wfull, 0);
+    if (w_res && px_first < npt) mbar_wait(&wfull, 0);
     for (int pt = px_first; pt < npt; pt += px_step, ++it) {
       const int acc = it & 1;
       mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (leader) {
-          const uint64_t wd = wdesc0 + (uint64_t)kb * w16, xd = xdesc0 + (uint64_t)stage * x16;
+          const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage) * w16, xd = xdesc0 + (uint64_t)stage * x16;
           for (int k = 0; k < ksteps; ++k) umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
           umma_commit(&empty[stage]);
         }
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream) {
-  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages);
+  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
 #define QNN_GT(M_, C_, S_)                                                                                 \
   if (mode == M_ && clamp == C_ && s8out == S_) {                                                          \

@@ -66,6 +66,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
 // the TMEM lanes (per-lane requantize constants in registers).
 struct GemmTParams {
   int BK, stages, num_kb, num_ch_tiles, num_px_tiles;
+  int w_res;             // weight block resident (else streamed per stage)
   uint32_t idesc;
   const int32_t* mult;   // [Kpad]
   const int32_t* rsh;    // [Kpad]
@@ -73,8 +74,8 @@ struct GemmTParams {
   int32_t zp_out, lo, hi;
   int dbg;   // QNN_GEMM_DEBUG (profiling): 1 skips the epilogue math, 2 the TMA stores
 };
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages);
-int gemm_t_max_stages(int BK, int num_kb);
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res);
+int gemm_t_max_stages(int BK, int num_kb, bool w_res);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream);
 
