@@ -782,9 +782,10 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   // requantize constants in its TMEM lane's registers.  QNN_NO_TRANS=1 keeps the pixel-major
   // kernel (A/B measurements).
   static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
+  static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
   if (!no_trans && !res && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
       d->groups == 1 && d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
-      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && d->K % 128 == 0 && d->K >= 256 && pl.out_cs % 16 == 0 &&
+      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && d->K % 128 == 0 && d->K >= kTransMinK && pl.out_cs % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(output) & 15) == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
     const int num_kb = pl.nchunks;   // one tap
     bool w_res = gemm_t_max_stages(pl.BK, num_kb, true) >= 3 &&

@@ -393,6 +393,7 @@ TRANS_CASES = [
     (3, 96, 5, 7, 384, "u8", "u8", True, True, "upward"),       # BK 32 x 3 chunks, clamp
     (2, 64, 6, 11, 256, "u8", "u8", True, False, "tonearest"),  # per-lane generic rounding
     (1, 640, 4, 4, 256, "u8", "s8", False, False, "upward"),    # 5 k-blocks of 128
+    (2, 256, 19, 21, 128, "u8", "u8", True, False, "upward"),   # one channel block (K 128)
     (2, 1024, 7, 9, 256, "u8", "u8", True, False, "upward"),    # weights streamed per stage
     (1, 2048, 5, 5, 512, "u8", "u8", True, False, "upward"),    # 16 streamed k-blocks
 ]
