@@ -475,7 +475,27 @@ __global__ void __launch_bounds__(256) requantize_fast_kernel(const __grid_const
   const long long nunits = p.count >> 9, gw = tid >> 5, nw = nthreads >> 5;
   const RqCh q0 = rq_ch<MODE>(p, 0);
   constexpr bool W16 = IN != DT_S32 && OUT != DT_S32;
-  for (long long u = gw; u < nunits; u += nw) {
+  // 8-bit inputs: two units per iteration, both loads issued before any math (one 16-B load
+  // per lane per unit is too little memory-level parallelism for HBM at one resident wave)
+  constexpr int UN = IN == DT_S32 ? 1 : 2;
+  long long u = gw;
+  for (; u + (UN - 1) * nw < nunits; u += UN * nw) {
+    int32_t x[UN][16], y[16];
+#pragma unroll
+    for (int v = 0; v < UN; ++v) load_il<IN, W16>(p.in, u + v * nw, lane, x[v]);
+#pragma unroll
+    for (int v = 0; v < UN; ++v) {
+      const long long uu = u + v * nw;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const RqCh q = CM == CM_VEC ? rq_ch<MODE>(p, il_channel<W16>(uu, j, lane, p.inner, p.cext)) : q0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) y[4 * j + k] = rq_fast<MODE>(x[v][4 * j + k], q, p.in_zp, p.out_zp);
+      }
+      store_il_sat<OUT, W16>(p.out, uu, lane, y);
+    }
+  }
+  for (; u < nunits; u += nw) {
     int32_t x[16], y[16];
     load_il<IN, W16>(p.in, u, lane, x);
 #pragma unroll
