@@ -782,10 +782,13 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   // requantize constants in its TMEM lane's registers.  QNN_NO_TRANS=1 keeps the pixel-major
   // kernel (A/B measurements).
   static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
+  // (K_out = 64 runs as half a 128-channel block: measured no faster than the pixel-major
+  // kernel on ResNet-50 layer1, so off unless QNN_TRANS_MINK=64)
   static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
   if (!no_trans && !res && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
       d->groups == 1 && d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
-      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && d->K % 128 == 0 && d->K >= kTransMinK && pl.out_cs % 16 == 0 &&
+      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
+      pl.out_cs % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(output) & 15) == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
     const int num_kb = pl.nchunks;   // one tap
     bool w_res = gemm_t_max_stages(pl.BK, num_kb, true) >= 3 &&
@@ -803,7 +806,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         tp.stages = stages;
         tp.num_kb = num_kb;
         tp.w_res = w_res;
-        tp.num_ch_tiles = d->K / 128;
+        tp.num_ch_tiles = (d->K + 127) / 128;
+        tp.Kout = d->K;
         tp.num_px_tiles = (int)((pl.M + 255) / 256);
         tp.idesc = make_idesc_i8(1, a_signed, 128, 256);   // A = s8 weights, B = activations
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);

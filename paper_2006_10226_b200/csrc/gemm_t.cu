@@ -177,8 +177,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
     // ---------------------------------------------------------------- epilogue
     const int quad = warp & 3, grp = warp >> 2;
     const int k = ch * kTBM + quad * 32 + lane;   // this lane's output channel
-    const int32_t M = p.mult[k], rsh = p.rsh[k];
-    const long long off = p.off64[k];
+    // (K_out = 64: the upper half of the 128-channel block is zero weights; its lanes compute
+    // nothing and their stores fall outside the output tensor, which TMA drops)
+    const bool quad_live = ch * kTBM + quad * 32 < p.Kout;
+    const int kk = k < p.Kout ? k : 0;
+    const int32_t M = p.mult[kk], rsh = p.rsh[kk];
+    const long long off = p.off64[kk];
     const bool fast = MODE == 0 && rsh >= 33 && rsh <= 52;
     int t = 0;
     long long K = 0;
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
       __syncwarp();
       // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
-      if (p.dbg & 1) {
+      if ((p.dbg & 1) || !quad_live) {
       } else if (all_fast) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0 && !(p.dbg & 2)) {
+      if (lane == 0 && quad_live && !(p.dbg & 2)) {
         tma_store_2d(&tmC, stage_out, ch * kTBM + quad * 32, pt * kTBN + grp * 64);
         bulk_commit();
       }

@@ -67,6 +67,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
 struct GemmTParams {
   int BK, stages, num_kb, num_ch_tiles, num_px_tiles;
   int w_res;             // weight block resident (else streamed per stage)
+  int Kout;              // output channels (a multiple of 128, or 64: half a block)
   uint32_t idesc;
   const int32_t* mult;   // [Kpad]
   const int32_t* rsh;    // [Kpad]

@@ -409,6 +409,28 @@ def test_wide_pointwise_channel_major(cfg):
     assert np.array_equal(got, want), mismatch_report(got, want)
 
 
+def test_pointwise_k64_channel_major_subprocess():
+    """QNN_TRANS_MINK=64: K_out = 64 on the channel-major kernel (half a channel block)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+for i, (C, adt, mode) in enumerate([(256, "u8", "upward"), (64, "s8", "tonearest")]):
+    case = gen.conv_case(1750 + i, 2, C, 13, 11, 64, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), 1, adt, "s8", rounding=mode)
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case)), i
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_TRANS_MINK="64"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
 def test_wide_pointwise_pixel_major_subprocess():
     """QNN_NO_TRANS=1 keeps the pixel-major kernel for the same shapes."""
     import os
