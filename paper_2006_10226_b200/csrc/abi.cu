@@ -785,7 +785,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   // (K_out = 64 runs as half a 128-channel block: measured no faster than the pixel-major
   // kernel on ResNet-50 layer1, so off unless QNN_TRANS_MINK=64)
   static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
-  if (!no_trans && !res && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
+  if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
       d->groups == 1 && d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
       (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
       pl.out_cs % 16 == 0 &&
@@ -795,11 +795,13 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
                  gemm_t_smem_bytes(pl.BK, num_kb, gemm_t_max_stages(pl.BK, num_kb, true), true) <= 226 * 1024;
     const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res);
     if (stages >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res) <= 226 * 1024) {
-      alignas(64) CUtensorMap tmX, tmW, tmC;
+      alignas(64) CUtensorMap tmX, tmW, tmC, tmR;
+      std::memset(&tmR, 0, sizeof(tmR));
       const int a_chan = d->C;
       bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, 256) &&
                  encode_2d(&tmW, pk + pl.pk_w, (uint64_t)pl.Cw, (uint64_t)pl.Kpad, (uint64_t)pl.Cw, pl.BK, 128) &&
-                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 64, false);
+                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 64, false) &&
+                 (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, 32, 64, false));
       if (okt) {
         GemmTParams tp{};
         tp.BK = pl.BK;
@@ -808,6 +810,13 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         tp.w_res = w_res;
         tp.num_ch_tiles = (d->K + 127) / 128;
         tp.Kout = d->K;
+        if (res) {
+          tp.has_res = 1;
+          tp.res_M = res_M;
+          tp.res_rsh = res_rsh;
+          tp.res_zp = res->zp;
+          tp.res_s8 = res->dtype == QNN_S8;
+        }
         tp.num_px_tiles = (int)((pl.M + 255) / 256);
         tp.idesc = make_idesc_i8(1, a_signed, 128, 256);   // A = s8 weights, B = activations
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
@@ -826,7 +835,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         int64_t qlo, qhi;
         dtype_range(pl.out_dt == DT_S8 ? QNN_S8 : QNN_U8, &qlo, &qhi);
         const bool clamp = pl.lo > qlo || pl.hi < qhi;
-        return cuda_status(launch_gemm_t(tmX, tmW, tmC, tp, pl.mode, clamp, pl.out_dt == DT_S8, grid, s));
+        return cuda_status(launch_gemm_t(tmX, tmW, tmC, tmR, tp, pl.mode, clamp, pl.out_dt == DT_S8, grid, s));
       }
     }
   }

@@ -55,6 +55,20 @@ __device__ __forceinline__ void store2(uint32_t a, int32_t y0, int32_t y1, int32
   sts_u8(a + 32, b2 >> 8);
 }
 
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// the residual byte requantized to the output scale with zero point 0 (reading R19: added
+// to the conv's requantized value before the clamp)
+template <int MODE>
+__device__ __forceinline__ int32_t res_term(const GemmTParams& p, uint32_t b) {
+  const int32_t x = (p.res_s8 ? (int32_t)(int8_t)b : (int32_t)b) - p.res_zp;
+  return (int32_t)rq_round((int64_t)x * p.res_M, p.res_rsh, MODE);
+}
+
 // hi32(v * M + K) (64-bit addend): one IMAD.WIDE
 __device__ __forceinline__ int32_t madwide_hi(int32_t v, int32_t M, long long K) {
   long long d;
@@ -80,10 +94,11 @@ int gemm_t_max_stages(int BK, int num_kb, bool w_res) {
   return s;
 }
 
-template <int MODE, bool CLAMP, bool S8OUT>
+template <int MODE, bool CLAMP, bool S8OUT, bool RES>
 __global__ void __launch_bounds__(kTThreads, 1)
     qnn_gemm_t_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmTParams p) {
+                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+                      const __grid_constant__ GemmTParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int BK = p.BK, stages = p.stages, num_kb = p.num_kb;
@@ -92,7 +107,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint8_t* sX = smem;                                  // stages x [256 pixels][BK]
   uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb (resident) or stages x [128 channels][BK]
   uint8_t* sOut = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // 16 x [64 pixels][32 channels]
-  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2], wfull;
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2], wfull, rbar[kTEpiWarps];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = kTEpiWarps, kMmaWarp = kTEpiWarps + 1;
@@ -103,6 +118,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmC);
+    if (RES) tma_prefetch_desc(&tmR);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -112,6 +128,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       mbar_init(&tempty[a], kTEpiWarps);
     }
     mbar_init(&wfull, 1);
+    for (int w = 0; w < kTEpiWarps; ++w) mbar_init(&rbar[w], 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(&tmem_slot, 512);
@@ -197,6 +214,18 @@ __global__ void __launch_bounds__(kTThreads, 1)
     int it = 0;
     for (int pt = px_first; pt < npt; pt += px_step, ++it) {
       const int acc = it & 1;
+      if (RES) {
+        // the residual tile (this warp's 64 pixels x 32 channels) lands in the staging tile
+        // itself; each lane then reads its channel's byte per pixel and overwrites it
+        if (lane == 0) {
+          bulk_wait_read<0>();   // the previous tile's store has read the staging tile
+          if (quad_live) {
+            mbar_arrive_expect_tx(&rbar[warp], kTStageOut);
+            tma_load_2d(stage_out, &tmR, &rbar[warp], ch * kTBM + quad * 32, pt * kTBN + grp * 64);
+          }
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 64);
@@ -209,9 +238,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&tempty[acc]);
-        bulk_wait_read<0>();   // the previous tile's store has read the staging tile
+        if (!RES) bulk_wait_read<0>();   // the previous tile's store has read the staging tile
       }
       __syncwarp();
+      if (RES && quad_live) mbar_wait(&rbar[warp], (uint32_t)(it & 1));
       // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
       if ((p.dbg & 1) || !quad_live) {
       } else if (all_fast) {
@@ -219,9 +249,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
         for (int h = 0; h < 2; ++h) {
           const uint32_t* v = h ? vb : va;
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            store2<CLAMP, S8OUT>(st_lane + (uint32_t)((h * 32 + j) * 32), madwide_hi((int32_t)v[j], M, K) >> t,
-                                 madwide_hi((int32_t)v[j + 1], M, K) >> t, p.lo, p.hi);
+          for (int j = 0; j < 32; j += 2) {
+            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
+            int32_t y0 = madwide_hi((int32_t)v[j], M, K) >> t, y1 = madwide_hi((int32_t)v[j + 1], M, K) >> t;
+            if (RES) {
+              y0 += res_term<MODE>(p, lds_u8(a));
+              y1 += res_term<MODE>(p, lds_u8(a + 32));
+            }
+            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
+          }
         }
       } else {
 #pragma unroll
@@ -238,7 +274,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
               y0 = rq_apply((long long)(int32_t)v[j] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
               y1 = rq_apply((long long)(int32_t)v[j + 1] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
             }
-            store2<CLAMP, S8OUT>(st_lane + (uint32_t)((h * 32 + j) * 32), y0, y1, p.lo, p.hi);
+            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
+            if (RES) {
+              y0 += res_term<MODE>(p, lds_u8(a));
+              y1 += res_term<MODE>(p, lds_u8(a + 32));
+            }
+            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
           }
         }
       }
@@ -262,27 +303,31 @@ __global__ void __launch_bounds__(kTThreads, 1)
 }
 
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
-                          const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream) {
+                          const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
+                          cudaStream_t stream) {
+  const bool res = p.has_res;
   const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
-#define QNN_GT(M_, C_, S_)                                                                                 \
-  if (mode == M_ && clamp == C_ && s8out == S_) {                                                          \
-    auto kern = qnn_gemm_t_kernel<M_, C_, S_>;                                                             \
+#define QNN_GT(M_, C_, S_, R_)                                                                             \
+  if (mode == M_ && clamp == C_ && s8out == S_ && res == R_) {                                             \
+    auto kern = qnn_gemm_t_kernel<M_, C_, S_, R_>;                                                         \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmemMax);  \
       if (e != cudaSuccess) return e;                                                                      \
       attr = true;                                                                                         \
     }                                                                                                      \
-    kern<<<grid, kTThreads, smem, stream>>>(tmX, tmW, tmC, p);                                             \
+    kern<<<grid, kTThreads, smem, stream>>>(tmX, tmW, tmC, tmR, p);                                        \
     count_launch();                                                                                        \
     const cudaError_t e = cudaGetLastError();                                                              \
     if (e != cudaSuccess && std::getenv("QNN_PLAN_TRACE"))                                                 \
       std::fprintf(stderr, "[qnn gemm_t] launch failed: %s\n", cudaGetErrorString(e));                    \
     return e;                                                                                              \
   }
-  QNN_GT(0, false, false) QNN_GT(0, false, true) QNN_GT(0, true, false) QNN_GT(0, true, true)
-  QNN_GT(1, false, false) QNN_GT(1, false, true) QNN_GT(1, true, false) QNN_GT(1, true, true)
+#define QNN_GT_R(M_, C_, S_) QNN_GT(M_, C_, S_, false) QNN_GT(M_, C_, S_, true)
+  QNN_GT_R(0, false, false) QNN_GT_R(0, false, true) QNN_GT_R(0, true, false) QNN_GT_R(0, true, true)
+  QNN_GT_R(1, false, false) QNN_GT_R(1, false, true) QNN_GT_R(1, true, false) QNN_GT_R(1, true, true)
+#undef QNN_GT_R
 #undef QNN_GT
   return cudaErrorInvalidValue;
 }

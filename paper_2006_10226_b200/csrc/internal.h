@@ -68,6 +68,8 @@ struct GemmTParams {
   int BK, stages, num_kb, num_ch_tiles, num_px_tiles;
   int w_res;             // weight block resident (else streamed per stage)
   int Kout;              // output channels (a multiple of 128, or 64: half a block)
+  int has_res;           // fused residual add (qnn_conv2d_packed_add): tmR + these
+  int32_t res_M, res_rsh, res_zp, res_s8;
   uint32_t idesc;
   const int32_t* mult;   // [Kpad]
   const int32_t* rsh;    // [Kpad]
@@ -78,7 +80,8 @@ struct GemmTParams {
 size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res);
 int gemm_t_max_stages(int BK, int num_kb, bool w_res);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
-                          const GemmTParams& p, int mode, bool clamp, bool s8out, int grid, cudaStream_t stream);
+                          const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
+                          cudaStream_t stream);
 
 struct GemmParams {
   int M, Nout;

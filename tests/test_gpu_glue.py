@@ -75,6 +75,10 @@ FUSED = [
     (2, 48, 9, 9, 96, 3, (2, 2), (1, 1, 1, 1), "s8", "s8", False, "tonearest"),
     (1, 128, 7, 7, 512, 1, (1, 1), (0, 0, 0, 0), "u8", "u8", False, "upward"),      # 2 N tiles
     (2, 16, 10, 10, 32, 3, (1, 1), (1, 1, 1, 1), "u8", "u8", True, "tonearest"),
+    # channel-major pointwise kernel with the residual tile staged by TMA
+    (3, 256, 9, 11, 1024, 1, (1, 1), (0, 0, 0, 0), "s8", "u8", True, "upward"),
+    (2, 128, 10, 10, 256, 1, (1, 1), (0, 0, 0, 0), "u8", "s8", False, "tonearest"),
+    (1, 1024, 5, 5, 256, 1, (1, 1), (0, 0, 0, 0), "u8", "u8", True, "upward"),      # streamed weights
 ]
 
 
