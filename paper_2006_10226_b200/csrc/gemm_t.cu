@@ -265,21 +265,23 @@ __global__ void __launch_bounds__(kTThreads, 1)
           const uint32_t* v = h ? vb : va;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            int32_t y0, y1;
+            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
+            int64_t z0, z1;   // exact: requantized value + zp_out (+ residual), clamped below
             if (fast) {
-              y0 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j] * M) + (unsigned long long)K) >> 32) >> t;
-              y1 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j + 1] * M) + (unsigned long long)K) >> 32) >>
+              z0 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j] * M) + (unsigned long long)K) >> 32) >> t;
+              z1 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j + 1] * M) + (unsigned long long)K) >> 32) >>
                    t;
             } else {
-              y0 = rq_apply((long long)(int32_t)v[j] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
-              y1 = rq_apply((long long)(int32_t)v[j + 1] + off, M, rsh, MODE, p.zp_out, p.lo, p.hi);
+              z0 = rq_round(((long long)(int32_t)v[j] + off) * M, rsh, MODE) + p.zp_out;
+              z1 = rq_round(((long long)(int32_t)v[j + 1] + off) * M, rsh, MODE) + p.zp_out;
             }
-            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
             if (RES) {
-              y0 += res_term<MODE>(p, lds_u8(a));
-              y1 += res_term<MODE>(p, lds_u8(a + 32));
+              z0 += res_term<MODE>(p, lds_u8(a));
+              z1 += res_term<MODE>(p, lds_u8(a + 32));
             }
-            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
+            const int32_t y0 = (int32_t)(z0 < p.lo ? p.lo : (z0 > p.hi ? p.hi : z0));
+            const int32_t y1 = (int32_t)(z1 < p.lo ? p.lo : (z1 > p.hi ? p.hi : z1));
+            store2<false, S8OUT>(a, y0, y1, p.lo, p.hi);
           }
         }
       }
