@@ -79,7 +79,7 @@ def main(rnd="r01"):
              f"{'kernel':62s} {'n':>4s} {'time_us':>10s} {'share':>7s} {'dram_MB':>9s}"]
     for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"{k:62s} {n:4d} {t / 1e3:10.1f} {t / tot:7.3f} {b / 1e6:9.1f}")
-    gemm = [x for x in step if "qnn_gemm_i8_kernel" in x["name"]]
+    gemm = [x for x in step if "qnn_gemm_i8_kernel" in x["name"] or "qnn_gemm_t_kernel" in x["name"]]
     per_launch = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in gemm) / max(1, len(gemm))
     lines.append("")
     lines.append(f"GEMM launches: {len(gemm)}; mean DRAM traffic per launch {per_launch / 1e6:.2f} MB; "
