@@ -47,6 +47,9 @@ __device__ __forceinline__ int32_t dwt_dp4a(uint32_t a, uint32_t w, int32_t c) {
 
 }  // namespace
 
+#ifndef QNN_DWT_UNROLL
+#define QNN_DWT_UNROLL 3   // (3: the three-row window rotation becomes register renaming)
+#endif
 constexpr int kDwtThreads = 256;
 
 // One band of a stage: items (channel group g, output column q), lanes on consecutive g.  An
@@ -75,7 +78,11 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
     uint32_t a = st_base + (uint32_t)(x * cs);
     uint8_t* dst = out + (long long)q * p.out_cstride;
     uint32_t T0[4], T1[4], T2[4];   // per-channel words of the last three input rows (bytes: 3 taps + junk)
+#if defined(QNN_DWT_NO_UNROLL)
 #pragma unroll 1
+#else
+#pragma unroll 3   // the three-row window rotation becomes register renaming
+#endif
     for (int ir = 0; ir < rows; ++ir, a += row_bytes) {
       const int h = h0 + ir;
       const bool row_ok = h >= 0 && h < p.H;
