@@ -81,7 +81,7 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
 #if defined(QNN_DWT_NO_UNROLL)
 #pragma unroll 1
 #else
-#pragma unroll 3   // the three-row window rotation becomes register renaming
+#pragma unroll(SH == 1 ? 3 : 2)   // the window rotation becomes register renaming
 #endif
     for (int ir = 0; ir < rows; ++ir, a += row_bytes) {
       const int h = h0 + ir;
