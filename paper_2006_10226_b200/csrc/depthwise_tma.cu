@@ -71,10 +71,14 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
   const long long ostride = (long long)p.Q * p.out_cstride;   // one output row
   uint8_t* out = reinterpret_cast<uint8_t*>(p.out) + ((long long)n * p.P + p0) * ostride + c0;
   const uint32_t st_base = smem_u32(st) + 4u * (uint32_t)g;
+  // band rows inside the image: ir in [ir_lo, ir_lo + nin) (one unsigned compare per row)
+  const int ir_lo = max(0, -h0);
+  const uint32_t nin = (uint32_t)max(0, min(rows, p.H - h0) - ir_lo);
+  const int pl = p.pl, Wd = p.W;
   for (int it = threadIdx.x; it < items; it += kDwtThreads) {
     const int q = it >> lg;   // (it % G == g: kDwtThreads % G == 0)
     const int x = q * SH;     // box column of the first tap (box starts at input column -pl)
-    const bool c0ok = x - p.pl >= 0, c2ok = x + 2 - p.pl < p.W;   // the middle tap is always inside
+    const bool c0ok = x - pl >= 0, c2ok = x + 2 - pl < Wd;   // the middle tap is always inside
     uint32_t a = st_base + (uint32_t)(x * cs);
     uint8_t* dst = out + (long long)q * p.out_cstride;
     uint32_t T0[4], T1[4], T2[4];   // per-channel words of the last three input rows (bytes: 3 taps + junk)
@@ -84,8 +88,7 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
 #pragma unroll(SH == 1 ? 3 : 2)   // the window rotation becomes register renaming
 #endif
     for (int ir = 0; ir < rows; ++ir, a += row_bytes) {
-      const int h = h0 + ir;
-      const bool row_ok = h >= 0 && h < p.H;
+      const bool row_ok = (uint32_t)(ir - ir_lo) < nin;
       uint32_t wv[3];
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[0]) : "r"(a));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[1]) : "r"(a + cs));
