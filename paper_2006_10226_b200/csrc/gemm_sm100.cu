@@ -379,7 +379,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int ab = o & ~3;
       const uint32_t sh8 = (uint32_t)(o - ab) * 8u;
       const bool border = o < 0 || o + SC > rowlen;
-      const int jlo = max(0, -o), jhi = min(SC, rowlen - o);
+      // byte masks of the 8 window words (bytes outside the row take the fill): computed only
+      // for the few border pixels (hoisted for every pixel, they cost ~150 instructions per tile)
+      uint32_t mk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mk[k] = 0xFFFFFFFFu;
+      if (border) {
+        const int jlo = max(0, -o), jhi = min(SC, rowlen - o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int l = min(max(jlo - 4 * k, 0), 4), h = min(max(jhi - 4 * k, 0), 4);
+          const uint32_t mh = h == 4 ? 0xFFFFFFFFu : ((1u << (8 * h)) - 1u);
+          const uint32_t ml = l == 4 ? 0xFFFFFFFFu : ((1u << (8 * l)) - 1u);
+          mk[k] = h > l ? (mh & ~ml) : 0u;
+        }
+      }
       // a_zpfill: output row p of this pixel, for the filter rows that fall outside the image
       const int h0 = p.a_zpfill ? ((ri - (int)fdiv((uint32_t)ri, p.fdP) * p.P) * p.sh - p.pt) : 0;
       const uint32_t fill = p.a_zpfill ? p.a_zp4 : 0u;
@@ -400,13 +414,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int k = 0; k < 8; ++k) wv[k] = __funnelshift_r(u[k], u[k + 1], sh8);
         if (border) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int l = min(max(jlo - 4 * k, 0), 4), h = min(max(jhi - 4 * k, 0), 4);
-            const uint32_t mh = h == 4 ? 0xFFFFFFFFu : ((1u << (8 * h)) - 1u);
-            const uint32_t ml = l == 4 ? 0xFFFFFFFFu : ((1u << (8 * l)) - 1u);
-            const uint32_t m = h > l ? (mh & ~ml) : 0u;
-            wv[k] = (wv[k] & m) | (fill & ~m);
-          }
+          for (int k = 0; k < 8; ++k) wv[k] = (wv[k] & mk[k]) | (fill & ~mk[k]);
         }
         if (p.a_zpfill) {
           const int hh = h0 + r * p.dil_h;
