@@ -81,6 +81,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Backoff variant for the many-warp waits off the critical path (epilogue warps waiting for an
+// accumulator, A-tile builders waiting for a stage): between polls the warp sleeps, so the
+// polling does not take issue slots from the working warps of its SM sub-partition (the
+// hinted try_wait alone still returned hundreds of times per tile: ncu, stem kernel).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  while (!done) {
+    __nanosleep(64);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
 // Busy-poll variant (no suspend-time hint) for short, latency-critical waits.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   asm volatile(
