@@ -1,0 +1,61 @@
+"""Pins the workload shape tables (`workloads/shapes.py`) to
+something other than themselves: torchvision's model definitions of the
+paper's three evaluation models (Table 2).  Every Conv2d of the
+torchvision model is recorded with a forward hook on one image, and the
+multiset of (C, K, H, W, R, S, stride, pad, groups) must equal the table's.
+Also pins the analytic weight count `tools/fp_baseline.py` reports (SURVEY
+§8f row f3: int8 weights are exactly 1/4 of fp32)."""
+import sys
+import os
+
+import pytest
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from workloads.shapes import inception_v3_convs, mobilenet_v2_convs, resnet50_convs, resnet50_fc  # noqa: E402
+
+tv = pytest.importorskip("torchvision")
+
+
+def _torch_convs(model, hw):
+    rec = []
+
+    def hook(mod, inp, out):
+        x = inp[0]
+        p = mod.padding
+        rec.append((mod.in_channels, mod.out_channels, x.shape[2], x.shape[3], mod.kernel_size[0],
+                    mod.kernel_size[1], tuple(mod.stride), (p[0], p[1], p[0], p[1]), mod.groups))
+
+    hs = [m.register_forward_hook(hook) for m in model.modules() if isinstance(m, torch.nn.Conv2d)]
+    with torch.no_grad():
+        model.eval()(torch.zeros(1, 3, hw, hw))
+    for h in hs:
+        h.remove()
+    return sorted(rec)
+
+
+def _table(convs):
+    return sorted((c.C, c.K, c.H, c.W, c.R, c.S, tuple(c.stride), tuple(c.pad), c.groups) for c in convs)
+
+
+def test_resnet50_shapes_match_torchvision():
+    assert _table(resnet50_convs()) == _torch_convs(tv.models.resnet50(), 224)
+
+
+def test_mobilenet_v2_shapes_match_torchvision():
+    assert _table(mobilenet_v2_convs()) == _torch_convs(tv.models.mobilenet_v2(), 224)
+
+
+def test_inception_v3_shapes_match_torchvision():
+    m = tv.models.inception_v3(init_weights=False, aux_logits=False)
+    assert _table(inception_v3_convs()) == _torch_convs(m, 299)
+
+
+def test_resnet50_weight_count_and_int8_ratio():
+    m = tv.models.resnet50()
+    n_tv = sum(p.numel() for p in m.parameters() if p.dim() > 1)     # conv + fc weights, no BN / bias
+    fin, fout = resnet50_fc()
+    n = sum(c.K * (c.C // c.groups) * c.R * c.S for c in resnet50_convs()) + fin * fout
+    assert n == n_tv == 25_502_912
+    assert 4 * n == sum(p.numel() * p.element_size() for p in m.parameters() if p.dim() > 1)
