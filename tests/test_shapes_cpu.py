@@ -59,3 +59,21 @@ def test_resnet50_weight_count_and_int8_ratio():
     n = sum(c.K * (c.C // c.groups) * c.R * c.S for c in resnet50_convs()) + fin * fout
     assert n == n_tv == 25_502_912
     assert 4 * n == sum(p.numel() * p.element_size() for p in m.parameters() if p.dim() > 1)
+
+
+def test_footprint_liveness_planner():
+    """tools/fp_baseline.py's buffer-liveness peak on a hand-checked chain:
+    a(u8 x100) -> b(u8 x50) -> c(s32 x10) -> a.  a stays live across the whole sequence (it is
+    rewritten last), so the peak is at the middle call: 100 + 50 + 40 bytes; as fp32 every
+    element takes 4 bytes: 400 + 200 + 40."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fp_baseline as fb
+    tr = fb._Trace()
+    a, b = torch.zeros(100, dtype=torch.uint8), torch.zeros(50, dtype=torch.uint8)
+    c = torch.zeros(10, dtype=torch.int32)
+    f = tr.wrap(lambda *x, **k: None)
+    f(a, out=b)
+    f(b, out=c)
+    f(c, out=a)
+    assert tr.peak_live() == 190 and tr.peak_live(as_fp32=True) == 640
+    assert tr.peak_live(exclude={a.untyped_storage().data_ptr()}) == 90

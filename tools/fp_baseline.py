@@ -12,12 +12,15 @@ max pool, 16 fused residual adds, avg pool, qnn.dense, dequantize) on this
 library.  Same batch, same f32 224x224 input resident in HBM, CUDA events.
 
 f3 (fig:memory): runtime memory footprint split into
-weights (parameters) and intermediate feature maps, int8 vs fp32.  Measured
-with the CUDA caching allocator: weights = bytes allocated while building the
-model (int8: packed weights + folded offsets / multipliers, before any
-activation buffer), feature maps = peak allocated during a forward minus
-weights minus the f32 input.  The analytic weight bytes (conv + fc weights
-only, no BN) come from `workloads.shapes` for reference.
+weights (parameters) and intermediate feature maps, int8 vs fp32.  fp arms:
+the CUDA caching allocator (weights = bytes allocated by the model, feature
+maps = peak allocated during a forward minus weights minus the input; cuDNN
+workspaces included).  int8 arm: weights = the prepacked buffers (weights,
+folded offsets, multipliers); feature maps = the peak live set over one traced
+forward (each buffer live from its first to its last use, i.e. what a
+graph-level planner reusing dead buffers holds) plus the conv workspaces.
+The analytic weight count (conv + fc weights only, no BN) comes from
+`workloads.shapes` (pinned to torchvision in tests/test_shapes_cpu.py).
 
 Prints one JSON line.  Usage: python tools/fp_baseline.py [--batch 256] [--steps 30]
 """
@@ -91,24 +94,78 @@ def fp_arm(mode, batch, steps, dev):
             "input_bytes": int(in_bytes)}
 
 
+class _Trace:
+    """Records, per library call of one forward, which storages it reads and which it writes."""
+
+    def __init__(self):
+        self.events = []     # (reads: {ptr: bytes}, writes: {ptr: bytes})
+
+    @staticmethod
+    def _tensors(obj, acc):
+        if isinstance(obj, torch.Tensor):
+            st = obj.untyped_storage()
+            acc[st.data_ptr()] = (st.nbytes(), obj.element_size())
+        elif isinstance(obj, (tuple, list)):
+            for o in obj:
+                _Trace._tensors(o, acc)
+        return acc
+
+    def wrap(self, fn):
+        def call(*args, **kw):
+            out = kw.get("out")
+            reads = self._tensors([a for a in args] + [v for k, v in kw.items() if k != "out"], {})
+            self.events.append((reads, self._tensors(out, {})))
+            return fn(*args, **kw)
+        return call
+
+    def peak_live(self, exclude=(), as_fp32=False):
+        """Peak bytes over the call sequence when each buffer lives from its first to its last use
+        (what a graph-level memory planner reusing dead buffers achieves).  as_fp32: the same graph
+        with every buffer holding 4-byte elements (the fp32 execution of the same call sequence)."""
+        first, last, size = {}, {}, {}
+        for i, (r, w) in enumerate(self.events):
+            for p, b in list(r.items()) + list(w.items()):
+                if p in exclude:
+                    continue
+                first.setdefault(p, i)
+                last[p] = i
+                size[p] = b[0] // b[1] * 4 if as_fp32 else b[0]
+        return max(sum(size[p] for p in size if first[p] <= i <= last[p]) for i in range(len(self.events)))
+
+
+class _QnnProxy:
+    def __init__(self, mod, tr):
+        self._mod, self._tr = mod, tr
+
+    def __getattr__(self, name):
+        f = getattr(self._mod, name)
+        return self._tr.wrap(f) if name.startswith("qnn_") else f
+
+
 def int8_arm(batch, steps, dev):
     import bench
     torch.cuda.empty_cache()
     torch.cuda.synchronize()
-    base = torch.cuda.memory_allocated()
     m = bench.resnet50_full_model(batch)
     net = bench.GpuResNet50Full(m, dev)
     torch.cuda.synchronize()
-    total_static = torch.cuda.memory_allocated() - base
-    # weights = packed per-layer state (everything the ops own); buffers are the activations
+    ops = list(net.ops.values()) + [net.fc]
+    packed = sum(o.packed.numel() for o in ops)
+    ws = sum(o.workspace.numel() for o in ops if o.workspace is not None)
     act = sum(t.numel() * t.element_size() for t in net.buf.values())
     act += sum(t.numel() * t.element_size() for t in (net.q_image, net.pool, net.gap, net.fc_out, net.logits))
     in_bytes = net.image_d.numel() * net.image_d.element_size()
-    w_bytes = total_static - act - in_bytes
-    torch.cuda.reset_peak_memory_stats()
+    # one traced forward: buffer liveness under the real call sequence
+    tr = _Trace()
+    real_ops, real_fc, real_q = dict(net.ops), net.fc, net.qnn
+    net.ops = {k: tr.wrap(v) for k, v in real_ops.items()}
+    net.fc = tr.wrap(real_fc)
+    net.qnn = _QnnProxy(real_q, tr)
     net.step()
     torch.cuda.synchronize()
-    peak = torch.cuda.max_memory_allocated() - base
+    net.ops, net.fc, net.qnn = real_ops, real_fc, real_q
+    ex = {net.image_d.untyped_storage().data_ptr()}
+    live, live32 = tr.peak_live(exclude=ex), tr.peak_live(exclude=ex, as_fp32=True)
     net.capture()
     for _ in range(3):
         net.replay()
@@ -121,10 +178,13 @@ def int8_arm(batch, steps, dev):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     res = {"images_per_s": round(batch / (ms / 1000.0), 1), "ms_per_step": round(ms, 4),
-           "weights_bytes": int(w_bytes), "feature_map_bytes": int(peak - w_bytes - in_bytes),
-           "feature_map_bytes_allocated": int(act), "input_bytes": int(in_bytes),
-           "note": "every intermediate buffer is allocated separately (no reuse), so feature maps are "
-                   "the sum over all layers, not the peak live set"}
+           "weights_bytes": int(packed), "workspace_bytes": int(ws), "feature_map_bytes": int(live + ws),
+           "feature_map_bytes_allocated": int(act),
+           "feature_map_bytes_same_graph_fp32": int(live32), "input_bytes": int(in_bytes), "library_calls": len(tr.events),
+           "note": "weights = prepacked buffers (weights + folded offsets + multipliers); feature maps = peak "
+                   "live set over the traced call sequence (buffers reused once dead, as a graph memory "
+                   "planner does) + conv workspaces; feature_map_bytes_allocated = what the bench's "
+                   "no-reuse allocation actually holds"}
     del net
     torch.cuda.empty_cache()
     return res
@@ -135,7 +195,8 @@ def analytic_weights():
     conv_params = sum(c.K * (c.C // c.groups) * c.R * c.S for c in resnet50_convs())
     fin, fout = resnet50_fc()
     n = conv_params + fin * fout
-    return {"params": n, "int8_bytes": n, "fp32_bytes": 4 * n}
+    bias = sum(c.K for c in resnet50_convs()) + fout
+    return {"params": n, "int8_bytes": n, "fp32_bytes": 4 * (n + bias)}
 
 
 def main():
@@ -159,7 +220,16 @@ def main():
             "feature_maps": round(100.0 * i8["feature_map_bytes"] / max(1, f["feature_map_bytes"]), 1),
             "total": round(100.0 * (i8["weights_bytes"] + i8["feature_map_bytes"]) /
                            (f["weights_bytes"] + f["feature_map_bytes"]), 1)}
-    res["analytic_weights"] = analytic_weights()
+    aw = analytic_weights()
+    res["analytic_weights"] = aw
+    res["footprint_int8_pct_of_fp32_same_graph"] = {
+        "weights": round(100.0 * i8["weights_bytes"] / aw["fp32_bytes"], 1),
+        "feature_maps": round(100.0 * i8["feature_map_bytes"] / i8["feature_map_bytes_same_graph_fp32"], 1),
+        "total": round(100.0 * (i8["weights_bytes"] + i8["feature_map_bytes"]) /
+                       (aw["fp32_bytes"] + i8["feature_map_bytes_same_graph_fp32"]), 1),
+        "note": "fp32 side: analytic conv+fc weights (+ fp32 bias) and the int8 forward's buffer "
+                "liveness with 4-byte elements; the cuDNN-measured split above also counts BN "
+                "parameters, cuDNN workspaces and the caching allocator's peak"}
     res["paper_context"] = {"speedup_vs_fp32": {"Xeon Cascade Lake": 2.35, "T4": 2.15, "Pi3": 1.35, "Pi4": 1.40},
                             "footprint_total_pct_servers": "26-33", "cite": "P:17, P:439-443, P:434"}
     print(json.dumps(res), flush=True)
