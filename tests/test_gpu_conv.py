@@ -17,7 +17,7 @@ import torch
 import oracle as orc
 from gpu_helpers import gpu_conv, mismatch_report, oracle_conv, oracle_conv_at
 from workloads import gen
-from workloads.shapes import mobilenet_v2_convs, resnet50_unique
+from workloads.shapes import inception_v3_convs, mobilenet_v2_convs, resnet50_unique
 
 pytestmark = pytest.mark.gpu
 
@@ -153,6 +153,65 @@ def test_resnet50_layers_batch64_sampled(layer, per_channel):
     idx[:8] = [0, 1, got.size - 1, got.size - 2, layer.K - 1, layer.K, got.size // 2, got.size - layer.K]
     want = oracle_conv_at(case, idx, layer.P, layer.Q)
     assert np.array_equal(got[idx], want), layer.name
+
+
+def _inception_unique():
+    out, seen = [], set()
+    for c in inception_v3_convs():
+        k = (c.C, c.K, c.H, c.W, c.R, c.S, c.stride, c.pad)
+        if k not in seen:
+            seen.add(k)
+            out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("layer", _inception_unique(), ids=lambda c: c.name)
+def test_inception_v3_layers_batch1_full(layer):
+    """BASELINE configs[4]'s Inception-v3 stack: every distinct conv shape (3x3/s2/p0 stems,
+    5x5/p2 with 25 border classes, 1x7 / 7x1 and 1x3 / 3x1 asymmetric padding), full compare."""
+    case = gen.conv_case(3000 + zlib.crc32(layer.name.encode()) % 1000, 1, layer.C, layer.H, layer.W, layer.K,
+                         layer.R, layer.S, layer.stride, layer.pad, (1, 1), 1, "u8", "s8", relu=layer.relu)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), layer.name + "\n" + mismatch_report(got, want)
+
+
+@pytest.mark.parametrize("layer", [c for c in _inception_unique() if c.name in
+                                   ("Conv2d_2b_3x3", "Mixed_5b.branch5x5_2", "Mixed_6b.branch7x7_2",
+                                    "Mixed_6b.branch7x7_3", "Mixed_7b.branch3x3_2a", "Mixed_7c.branch1x1")],
+                         ids=lambda c: c.name)
+def test_inception_v3_layers_batch64_sampled(layer):
+    """Full-size (batch 64) Inception-v3 launches, 4096 sampled outputs vs the oracle."""
+    case = gen.conv_case(4000 + zlib.crc32(layer.name.encode()) % 1000, 64, layer.C, layer.H, layer.W, layer.K,
+                         layer.R, layer.S, layer.stride, layer.pad, (1, 1), 1, "u8", "s8", relu=layer.relu)
+    _, _, y = gpu_conv(case)
+    got = y.cpu().numpy().reshape(-1)
+    idx = np.random.default_rng(5).choice(got.size, 4096, replace=False)
+    idx[:6] = [0, 1, got.size - 1, layer.K - 1, layer.K, got.size - layer.K]
+    want = oracle_conv_at(case, idx, layer.P, layer.Q)
+    assert np.array_equal(got[idx], want), layer.name
+
+
+def _mobilenet_dense_unique():
+    out, seen = [], set()
+    for c in mobilenet_v2_convs():
+        k = (c.C, c.K, c.H, c.W, c.R, c.S, c.stride, c.act6, c.relu)
+        if c.groups == 1 and k not in seen:
+            seen.add(k)
+            out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("layer", _mobilenet_dense_unique(), ids=lambda c: c.name)
+def test_mobilenet_v2_pointwise_batch2_full(layer):
+    """BASELINE configs[2]'s non-depthwise MobileNet-v2 convs (3x3/s2 stem, 1x1 expand with
+    ReLU6 as an output-domain clamp, 1x1 linear project, last 1x1), full compare at batch 2."""
+    case = gen.conv_case(5000 + zlib.crc32(layer.name.encode()) % 1000, 2, layer.C, layer.H, layer.W, layer.K,
+                         layer.R, layer.S, layer.stride, layer.pad, (1, 1), 1, "u8", "s8", relu=layer.relu,
+                         act6=layer.act6)
+    _, _, y = gpu_conv(case)
+    got, want = y.cpu().numpy(), oracle_conv(case)
+    assert np.array_equal(got, want), layer.name + "\n" + mismatch_report(got, want)
 
 
 def _dw_layers():
