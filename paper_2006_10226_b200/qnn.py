@@ -318,6 +318,19 @@ def qnn_requantize(x: torch.Tensor, in_scales, in_zp: int, out_scale: float, out
     return out
 
 
+def legalize_s8_weights(w: torch.Tensor, zp_W: int, stream=None) -> tuple[torch.Tensor, int]:
+    """QNN Legalize for u8 x u8 convs: represent the u8 weights
+    as s8 by inserting a requantize before the weight operand, Q_W' = Q_W - 128, and shift the
+    zero point, zp_W' = zp_W - 128.  (Q_W - zp_W) is unchanged, so Eq. 3 gives the same Q_C.
+    Runs as one qnn_requantize launch (scales 1, in_zp zp_W, out_zp zp_W - 128, s8 out: exact,
+    no rounding).  tcgen05 takes u8 x u8 natively, so this is the alternative lowering, not a
+    requirement; the parity tests run both."""
+    if w.dtype != torch.uint8:
+        raise QnnError("legalize_s8_weights: weights must be u8")
+    zp2 = int(zp_W) - 128
+    return qnn_requantize(w, [1.0], int(zp_W), 1.0, zp2, "s8", stream=stream), zp2
+
+
 def qnn_quantize(x: torch.Tensor, scales, zero_points, out_dtype="u8", axis=-1, out=None, stream=None):
     odt = _dtcode(out_dtype)
     if out is None:

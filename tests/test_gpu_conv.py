@@ -535,3 +535,33 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_MMA2="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("cfg", [
+    (2, 64, 11, 9, 64, 3, 3, (1, 1), (1, 1, 1, 1), 117),
+    (2, 96, 14, 14, 300, 3, 3, (2, 2), (0, 1, 1, 0), 131),
+    (1, 256, 14, 14, 256, 1, 1, (1, 1), (0, 0, 0, 0), 0),
+    (1, 64, 56, 56, 64, 3, 3, (1, 1), (1, 1, 1, 1), 255),
+])
+def test_legalize_u8_weights_to_s8(cfg):
+    """SURVEY §8f row f4, the VNNI Legalize: u8 x u8 weights re-expressed as s8 with
+    zp_W - 128 by one qnn_requantize launch give the same bytes as the direct u8 x u8 lowering,
+    and both equal the oracle of the original (u8 x u8) problem."""
+    from paper_2006_10226_b200 import PackedConv2d
+    from paper_2006_10226_b200.qnn import legalize_s8_weights
+    N, C, H, W, K, R, S, st, pad, zpW = cfg
+    case = gen.conv_case(7000 + K, N, C, H, W, K, R, S, st, pad, (1, 1), 1, "u8", "u8", zp_W=zpW, per_channel=False)
+    want = oracle_conv(case)
+    w_d = torch.from_numpy(case.W).cuda()
+    w8, zp2 = legalize_s8_weights(w_d, zpW)
+    torch.cuda.synchronize()
+    assert w8.dtype == torch.int8 and zp2 == zpW - 128
+    assert np.array_equal(w8.cpu().numpy().astype(np.int16), case.W.astype(np.int16) - 128)
+    x = torch.from_numpy(case.A).cuda()
+    ys = []
+    for wt, zp in ((w_d, zpW), (w8, zp2)):
+        op = PackedConv2d(N, H, W, C, wt, torch.from_numpy(case.bias).cuda(), case.zp_A, zp, case.s_A, case.s_W,
+                          case.out_params(), case.stride, case.pad, case.dil, 1)
+        ys.append(op(x).cpu().numpy())
+    assert np.array_equal(ys[0], want), mismatch_report(ys[0], want)
+    assert np.array_equal(ys[1], want), mismatch_report(ys[1], want)
