@@ -222,10 +222,49 @@ __global__ void pixel_sums_kernel(const uint8_t* __restrict__ in, int a_signed, 
   pixsum[pix] = s;
 }
 
+// Coalesced variant for C % 16 == 0 with C / 16 a power of two: gl = min(C/16, 32) consecutive
+// lanes share one pixel (a warp reads 512 contiguous bytes per load when the pitch is C), each
+// lane sums its 16-byte chunks with dp4a, and the group reduces with xor shuffles.
+__global__ void pixel_sums_vec_kernel(const uint8_t* __restrict__ in, int a_signed, long long in_cstride, int G,
+                                      int gl, long long npix, int32_t* __restrict__ pixsum) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long pix = t / gl;
+  const int sub = (int)(t % gl);
+  int32_t s = 0;
+  if (pix < npix) {
+    const uint4* a = reinterpret_cast<const uint4*>(in + pix * in_cstride);
+    for (int k = sub; k < G; k += gl) {
+      const uint4 v = __ldg(a + k);
+      if (a_signed) {
+        s = __dp4a((int)v.x, 0x01010101, s);
+        s = __dp4a((int)v.y, 0x01010101, s);
+        s = __dp4a((int)v.z, 0x01010101, s);
+        s = __dp4a((int)v.w, 0x01010101, s);
+      } else {
+        s = (int32_t)__dp4a(v.x, 0x01010101u, (uint32_t)s);
+        s = (int32_t)__dp4a(v.y, 0x01010101u, (uint32_t)s);
+        s = (int32_t)__dp4a(v.z, 0x01010101u, (uint32_t)s);
+        s = (int32_t)__dp4a(v.w, 0x01010101u, (uint32_t)s);
+      }
+    }
+  }
+  for (int o = gl >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (sub == 0 && pix < npix) pixsum[pix] = s;
+}
+
 cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
                               int32_t* pixsum, cudaStream_t s) {
-  pixel_sums_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride, C,
-                                                                    npix, pixsum);
+  const int G = C / 16;
+  if (C % 16 == 0 && G > 0 && (G & (G - 1)) == 0 && (in_cstride & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    const int gl = G < 32 ? G : 32;
+    const long long threads = npix * gl;
+    pixel_sums_vec_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride,
+                                                                           G, gl, npix, pixsum);
+  } else {
+    pixel_sums_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride, C,
+                                                                      npix, pixsum);
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -66,6 +66,10 @@ SWEEP = [
     (1, 64, 8, 8, 1000, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 0, "u8", True),    # K=1000 tail
     (2, 32, 10, 10, 64, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "u8", "s8", 0, "s32", True),   # raw int32
     (1, 16, 5, 5, 16, 5, 5, (1, 1), (0, 0, 0, 0), (1, 1), "u8", "s8", 3, "s32", True),     # 1x1 output, raw
+    # Term-3 pixel sums on the coalesced path (C / 16 a power of two: 1, 16, 128 chunks per pixel)
+    (2, 256, 7, 9, 64, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "s8", "u8", 77, "u8", False),
+    (1, 2048, 5, 5, 32, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "s8", "s8", -5, "s8", True),
+    (3, 16, 6, 7, 16, 3, 3, (2, 2), (1, 1, 1, 1), (1, 1), "u8", "s8", 9, "u8", True),
 ]
 
 
