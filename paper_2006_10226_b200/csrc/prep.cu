@@ -224,32 +224,51 @@ __global__ void pixel_sums_kernel(const uint8_t* __restrict__ in, int a_signed, 
 
 // Coalesced variant for C % 16 == 0 with C / 16 a power of two: gl = min(C/16, 32) consecutive
 // lanes share one pixel (a warp reads 512 contiguous bytes per load when the pitch is C), each
-// lane sums its 16-byte chunks with dp4a, and the group reduces with xor shuffles.
+// lane sums its 16-byte chunks with dp4a, and the group reduces with xor shuffles.  A block
+// covers kPsUnroll x (256 / gl) pixels; each thread issues its kPsUnroll loads before any math
+// (bytes in flight for HBM latency).
+constexpr int kPsUnroll = 4;
+
+__device__ __forceinline__ int32_t dp4a_sum4(uint4 v, int32_t s, int a_signed) {
+  if (a_signed) {
+    s = __dp4a((int)v.x, 0x01010101, s);
+    s = __dp4a((int)v.y, 0x01010101, s);
+    s = __dp4a((int)v.z, 0x01010101, s);
+    return __dp4a((int)v.w, 0x01010101, s);
+  }
+  s = (int32_t)__dp4a(v.x, 0x01010101u, (uint32_t)s);
+  s = (int32_t)__dp4a(v.y, 0x01010101u, (uint32_t)s);
+  s = (int32_t)__dp4a(v.z, 0x01010101u, (uint32_t)s);
+  return (int32_t)__dp4a(v.w, 0x01010101u, (uint32_t)s);
+}
+
 __global__ void pixel_sums_vec_kernel(const uint8_t* __restrict__ in, int a_signed, long long in_cstride, int G,
                                       int gl, long long npix, int32_t* __restrict__ pixsum) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long pix = t / gl;
-  const int sub = (int)(t % gl);
-  int32_t s = 0;
-  if (pix < npix) {
-    const uint4* a = reinterpret_cast<const uint4*>(in + pix * in_cstride);
-    for (int k = sub; k < G; k += gl) {
-      const uint4 v = __ldg(a + k);
-      if (a_signed) {
-        s = __dp4a((int)v.x, 0x01010101, s);
-        s = __dp4a((int)v.y, 0x01010101, s);
-        s = __dp4a((int)v.z, 0x01010101, s);
-        s = __dp4a((int)v.w, 0x01010101, s);
-      } else {
-        s = (int32_t)__dp4a(v.x, 0x01010101u, (uint32_t)s);
-        s = (int32_t)__dp4a(v.y, 0x01010101u, (uint32_t)s);
-        s = (int32_t)__dp4a(v.z, 0x01010101u, (uint32_t)s);
-        s = (int32_t)__dp4a(v.w, 0x01010101u, (uint32_t)s);
-      }
-    }
+  const int per_pass = blockDim.x / gl;   // pixels per block per unroll step
+  const int sub = threadIdx.x % gl;
+  const long long pix0 = (long long)blockIdx.x * per_pass * kPsUnroll + threadIdx.x / gl;
+  int32_t s[kPsUnroll];
+  uint4 v[kPsUnroll];
+#pragma unroll
+  for (int u = 0; u < kPsUnroll; ++u) {
+    s[u] = 0;
+    v[u] = make_uint4(0u, 0u, 0u, 0u);
   }
-  for (int o = gl >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (sub == 0 && pix < npix) pixsum[pix] = s;
+  for (int k = sub; k < G; k += gl) {
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) {
+      const long long pix = pix0 + (long long)u * per_pass;
+      if (pix < npix) v[u] = __ldg(reinterpret_cast<const uint4*>(in + pix * in_cstride) + k);
+    }
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) s[u] = dp4a_sum4(v[u], s[u], a_signed);
+  }
+#pragma unroll
+  for (int u = 0; u < kPsUnroll; ++u) {
+    for (int o = gl >> 1; o > 0; o >>= 1) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+    const long long pix = pix0 + (long long)u * per_pass;
+    if (sub == 0 && pix < npix) pixsum[pix] = s[u];
+  }
 }
 
 cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
@@ -258,8 +277,8 @@ cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride
   if (C % 16 == 0 && G > 0 && (G & (G - 1)) == 0 && (in_cstride & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
     const int gl = G < 32 ? G : 32;
-    const long long threads = npix * gl;
-    pixel_sums_vec_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride,
+    const long long per_block = (long long)(256 / gl) * kPsUnroll;
+    pixel_sums_vec_kernel<<<(unsigned)((npix + per_block - 1) / per_block), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride,
                                                                            G, gl, npix, pixsum);
   } else {
     pixel_sums_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride, C,
