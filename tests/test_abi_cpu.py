@@ -156,3 +156,13 @@ def test_no_cpu_fallback_without_library(qlib, tmp_path, monkeypatch):
     monkeypatch.delenv("QNN_AUTOBUILD", raising=False)
     with pytest.raises(q.QnnError):
         q.lib()
+
+
+def test_legalize_rejects_non_u8_weights():
+    """The Legalize applies to u8 weights only; the dtype check happens in the
+    binding before any launch, so it is testable without a GPU."""
+    import torch
+
+    from paper_2006_10226_b200.qnn import QnnError, legalize_s8_weights
+    with pytest.raises(QnnError):
+        legalize_s8_weights(torch.zeros(4, 1, 1, 16, dtype=torch.int8), 0)
