@@ -217,6 +217,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
       K = (long long)((unsigned long long)off * (unsigned long long)(long long)M + (c64 << 32));
     }
     const bool all_fast = __all_sync(0xffffffffu, fast);
+    // 32-bit form of the fast path: with |acc| <= KK * 255 * 255 (any operand dtypes / zps) and
+    // |off| below 2^31 minus that bound, acc + off is exact in int32, and since the rounding
+    // constant c64 has no bits below 2^32,  hi64((acc + off) * M + c64 * 2^32) = hi32((acc + off) * M) + c64:
+    // one IMAD.HI with a 32-bit addend instead of a 64-bit multiply-add with carry.
+    const long long acc_bound = (long long)p.num_kb * p.BK * 65025LL;
+    const bool fast32 = fast && (off < 0 ? -off : off) < (1LL << 31) - 1 - acc_bound;
+    const int32_t off32 = (int32_t)off;
+    const int32_t c32 = fast ? (int32_t)((1 << (t - 1)) + p.zp_out * (1 << t)) : 0;
+    const bool all_fast32 = __all_sync(0xffffffffu, fast32) && !(p.dbg & 4);
     uint8_t* stage_out = sOut + warp * kTStageOut;
     const uint32_t st_lane = smem_u32(stage_out) + (uint32_t)lane;
     int it = 0;
@@ -252,6 +261,23 @@ __global__ void __launch_bounds__(kTThreads, 1)
       if (RES && quad_live) mbar_wait(&rbar[warp], (uint32_t)(it & 1));
       // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
       if ((p.dbg & 1) || !quad_live) {
+      } else if (all_fast32) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* v = h ? vb : va;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
+            int32_t y0 = __mulhi((int32_t)v[j] + off32, M) + c32, y1 = __mulhi((int32_t)v[j + 1] + off32, M) + c32;
+            y0 >>= t;
+            y1 >>= t;
+            if (RES) {
+              y0 += res_term<MODE>(p, lds_u8(a));
+              y1 += res_term<MODE>(p, lds_u8(a + 32));
+            }
+            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
+          }
+        }
       } else if (all_fast) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
