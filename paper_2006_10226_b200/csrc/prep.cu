@@ -222,7 +222,7 @@ __global__ void pixel_sums_kernel(const uint8_t* __restrict__ in, int a_signed, 
   pixsum[pix] = s;
 }
 
-// Coalesced variant for C % 16 == 0 with C / 16 a power of two: gl = min(C/16, 32) consecutive
+// Coalesced variant for C % 16 == 0: gl = min(pow2floor(C/16), 32) consecutive
 // lanes share one pixel (a warp reads 512 contiguous bytes per load when the pitch is C), each
 // lane sums its 16-byte chunks with dp4a, and the group reduces with xor shuffles.  A block
 // covers kPsUnroll x (256 / gl) pixels; each thread issues its kPsUnroll loads before any math
@@ -274,9 +274,9 @@ __global__ void pixel_sums_vec_kernel(const uint8_t* __restrict__ in, int a_sign
 cudaError_t launch_pixel_sums(const void* in, int a_signed, long long in_cstride, int C, long long npix,
                               int32_t* pixsum, cudaStream_t s) {
   const int G = C / 16;
-  if (C % 16 == 0 && G > 0 && (G & (G - 1)) == 0 && (in_cstride & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
-    const int gl = G < 32 ? G : 32;
+  if (C % 16 == 0 && G > 0 && (in_cstride & 15) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    int gl = 1;   // lanes per pixel: the largest power of two <= min(G, 32) (lanes loop over the rest)
+    while (gl * 2 <= G && gl < 32) gl *= 2;
     const long long per_block = (long long)(256 / gl) * kPsUnroll;
     pixel_sums_vec_kernel<<<(unsigned)((npix + per_block - 1) / per_block), 256, 0, s>>>((const uint8_t*)in, a_signed, in_cstride,
                                                                            G, gl, npix, pixsum);

@@ -70,6 +70,9 @@ SWEEP = [
     (2, 256, 7, 9, 64, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "s8", "u8", 77, "u8", False),
     (1, 2048, 5, 5, 32, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), "s8", "s8", -5, "s8", True),
     (3, 16, 6, 7, 16, 3, 3, (2, 2), (1, 1, 1, 1), (1, 1), "u8", "s8", 9, "u8", True),
+    # ... and with C / 16 not a power of two (Inception-v3 widths: 12 and 48 chunks per pixel)
+    (1, 192, 9, 11, 64, 1, 7, (1, 1), (0, 3, 0, 3), (1, 1), "u8", "u8", 100, "u8", False),
+    (2, 768, 5, 5, 32, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), "s8", "s8", 4, "s8", True),
 ]
 
 
