@@ -77,3 +77,26 @@ def test_footprint_liveness_planner():
     f(c, out=a)
     assert tr.peak_live() == 190 and tr.peak_live(as_fp32=True) == 640
     assert tr.peak_live(exclude={a.untyped_storage().data_ptr()}) == 90
+
+
+def test_fp_baseline_bn_folding_preserves_the_forward():
+    """tools/fp_baseline.py folds BN into the convs of the cuDNN comparison arm (row f2); the
+    folded model must compute the same function (fp32 rounding only) and contain no BN."""
+    import copy
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fp_baseline as fb
+    torch.manual_seed(0)
+    m = tv.models.resnet50().eval()
+    for mod in m.modules():
+        if isinstance(mod, torch.nn.BatchNorm2d):
+            mod.running_mean.uniform_(-0.5, 0.5)
+            mod.running_var.uniform_(0.5, 2.0)
+            mod.weight.data.uniform_(0.5, 1.5)
+            mod.bias.data.uniform_(-0.2, 0.2)
+    f = fb._fold_bn(copy.deepcopy(m))
+    assert not any(isinstance(q, torch.nn.BatchNorm2d) for q in f.modules())
+    x = torch.randn(2, 3, 224, 224)
+    with torch.no_grad():
+        y0, y1 = m(x), f(x)
+    assert (y0 - y1).abs().max().item() <= 1e-5 * max(1.0, y0.abs().max().item())
