@@ -9,11 +9,13 @@ One step = one pass of the whole hot path over one batch (per GPU):
 Glue ops that are not on the path (max pool, residual add, global avg pool)
 are not run; layers fed by them read persistent synthetic buffers.
 
-Contract: ``python bench.py --gpus N --steps K --warmup W`` (torchrun for N>1,
-one rank per GPU, batch sharded: every rank processes its own 256 images,
-weights replicated, no collective on the data path).  Rank 0 prints ONE JSON
-line.  ``--impl reference`` times the CPU oracle (the reference arm of this
-tier) on a bounded sample of the same workload.
+Contract: ``python bench.py --gpus N --steps K --warmup W``.  configs[4] is a batch of 256
+images SHARDED over the N GPUs (strong scaling: rank r takes images shard_range(256, r, N),
+weights replicated, no collective on the data path; time = max over ranks).  Without
+torchrun, ``--gpus N > 1`` launches the N ranks itself (torch.distributed.run, 127.0.0.1).
+For N > 1 the line also carries a weak-scaling figure (256 images per GPU).  Rank 0 prints
+ONE JSON line.  ``--impl reference`` times the CPU oracle (the reference arm of this tier)
+on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -85,6 +87,18 @@ def resnet50_model(batch: int, seed: int = 4000):
     image = gen.rng(seed + 98).standard_normal((batch, 224, 224, 3)).astype(np.float32)
     return dict(specs=specs, weights=weights, biases=biases, fresh=fresh, fc=fc, image=image,
                 img_scale=img_scale, img_zp=img_zp)
+
+
+def shard_model(model, lo: int, hi: int):
+    """Rank's slice [lo, hi) of a batch built by resnet50_model (images are
+    independent; weights, biases and scales are shared, every per-image array is sliced), so
+    the ranks' outputs concatenate to the 1-GPU output of the same global batch."""
+    from dataclasses import replace
+    n = hi - lo
+    fc = dict(model["fc"])
+    fc["A"] = model["fc"]["A"][lo:hi]
+    return dict(model, specs=[replace(sp, N=n) for sp in model["specs"]],
+                fresh={k: v[lo:hi] for k, v in model["fresh"].items()}, fc=fc, image=model["image"][lo:hi])
 
 
 class GpuResNet50:
@@ -210,6 +224,10 @@ def resnet50_full_model(batch: int, seed: int = 5000, fused: bool = True):
               bias=g.integers(-4096, 4097, size=fout).astype(np.int32))
     image = gen.rng(seed + 98).standard_normal((batch, 224, 224, 3)).astype(np.float32)
     return dict(layers=layers, blocks=blocks, fc=fc, image=image, img_scale=img_scale, img_zp=img_zp, batch=batch)
+
+
+def shard_full_model(m, lo: int, hi: int):
+    return dict(m, image=m["image"][lo:hi], batch=hi - lo)
 
 
 class GpuResNet50Full:
@@ -427,23 +445,75 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- main
+def _spawn_ranks(args) -> int:
+    """--gpus N > 1 without torchrun: launch the N ranks ourselves (one process per GPU)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _peaks():
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    mma = {}
+    try:
+        mma = json.load(open(os.path.join(ROOT, "profiles", "mma_peak.json")))
+    except (OSError, ValueError):
+        pass
+    return peaks, mma
+
+
+def _layer_roofline_us(macs: float, nbytes: float, tc_tops: float, hbm_gbs: float) -> float:
+    """min-time of one launch on the measured roofline: max(ops / TC peak, bytes / HBM peak)."""
+    return max(2.0 * macs / (tc_tops * 1e12), nbytes / (hbm_gbs * 1e9)) * 1e6
+
+
+def _time_replays(torch, replay, steps, world, dist, dev):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        replay()
+    t1.record()
+    torch.cuda.synchronize()
+    from paper_2006_10226_b200.sharding import max_over_ranks
+    return max_over_ranks(t0.elapsed_time(t1), dist if world > 1 else None, dev)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--batch", type=int, default=256, help="images per GPU per step")
+    ap.add_argument("--global-batch", type=int, default=256,
+                    help="configs[4]: images per step over ALL GPUs (strong scaling: 256 / N per GPU)")
     ap.add_argument("--impl", default="qnn", choices=["qnn", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-full-network", dest="full_network", action="store_false",
                     help="skip the full-forward (glue ops) measurement")
+    ap.add_argument("--no-weak", dest="weak", action="store_false", help="skip the weak-scaling figure (N > 1)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "contract: at least 3 warm-up steps"
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -451,39 +521,31 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2006_10226_b200.sharding import max_over_ranks
+    from paper_2006_10226_b200.sharding import max_over_ranks, shard_range
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    model = resnet50_model(args.batch)
+    G = args.global_batch
+    lo, hi = shard_range(G, rank, world)
+    gmodel = resnet50_model(G)
+    model = shard_model(gmodel, lo, hi)
+    batch = hi - lo
     net = GpuResNet50(model, dev)
     net.capture()
     for _ in range(args.warmup):
         net.replay()
     torch.cuda.synchronize()
 
-    # ---------------- timed region: K graph replays, inputs resident in HBM
+    # ---------------- timed region: K graph replays, inputs resident in HBM (strong scaling)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(args.steps):
-        net.replay()
-    t1.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms = _time_replays(torch, net.replay, args.steps, world, dist, dev)
     clk = clocks.stop()
-    ms = max_over_ranks(t0.elapsed_time(t1), dist if world > 1 else None, dev)
     ms_per_step = ms / args.steps
-    images = args.batch * world * args.steps
-    value = images / (ms / 1000.0)
+    value = G * args.steps / (ms / 1000.0)
 
     # ---------------- e2e: host f32 image in (pinned H2D) -> graph -> logits out (D2H), same metric
     host_in = torch.from_numpy(model["image"]).pin_memory()
@@ -521,7 +583,7 @@ def main():
     e1.record(cstream)
     torch.cuda.synchronize()
     ems = max_over_ranks(e0.elapsed_time(e1), dist if world > 1 else None, dev)
-    e2e_value = args.batch * world * e2e_steps / (ems / 1000.0)
+    e2e_value = G * e2e_steps / (ems / 1000.0)
     h2d = host_in.numel() * 4
     d2h = host_out.numel() * 4
 
@@ -552,7 +614,8 @@ def main():
     layer_ms /= args.breakdown_steps
     fc_ms /= args.breakdown_steps
     macs = [sp.macs() for sp in net.stack.specs]
-    fc_macs = model["fc"]["A"].shape[0] * model["fc"]["W"].shape[0] * model["fc"]["W"].shape[1]
+    fcW = model["fc"]["W"]
+    fc_macs = batch * fcW.shape[0] * fcW.shape[1]
     # GEMM time of a step: the 54 GEMM launches captured as ONE graph (exactly the step's
     # kernels minus quantize/dequantize), replayed back to back between two events
     gg = torch.cuda.CUDAGraph()
@@ -572,45 +635,63 @@ def main():
     gemm_ms = g0.elapsed_time(g1) / reps
     gemm_ops = 2.0 * (sum(macs) + fc_macs)
     gemm_launches = nl + 1
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
+    peaks, mma = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    bf16_burst = peaks.get("bf16_tflops", 1590.0)
     bf16_sus = peaks.get("bf16_tflops_sustained", 1400.0)
-    int8_peak = 2.0 * bf16_sus       # nominal int8:bf16 = 4.5:2.25 (B200_PROFILING.md) x measured sustained bf16
+    # the guide's rule: int8 peak = measured bf16 x nominal 4.5/2.25; the burst figure when the
+    # timed region ran at (near) max SM clock, the sustained one when it ran throttled
+    sm_mhz, sm_max = clk.get("sm_mhz"), clk.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    burst = sm_mhz is None or sm_mhz >= 0.95 * sm_max
+    int8_peak = 2.0 * (bf16_burst if burst else bf16_sus)
     achieved = gemm_ops / (gemm_ms / 1000.0) / 1e12
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
-        if tr.get("batch") == args.batch:
+        if tr.get("batch") == batch:
             traffic = tr.get("bytes_per_launch")
     except (OSError, ValueError):
         pass
     step_ops = 2.0 * (net.stack.total_macs() + fc_macs)
-    conv_tops = step_ops / (ms_per_step / 1000.0) / 1e12
+    conv_tops = step_ops / (ms_per_step / 1000.0) / 1e12 * world
+    # per-layer roofline (algorithmic bytes = input once + weights + output + 12 B/channel)
+    layer_bytes = [sp.N * sp.H * sp.W * sp.C + sp.K * sp.C * sp.R * sp.S + sp.N * sp.P * sp.Q * sp.K + 12 * sp.K
+                   for sp in net.stack.specs]
+    roof_us = [_layer_roofline_us(m, b, int8_peak, hbm) for m, b in zip(macs, layer_bytes)]
+    fc_bytes = batch * fcW.shape[1] + fcW.size + batch * fcW.shape[0] * 4 + 12 * fcW.shape[0]
+    fc_roof_us = _layer_roofline_us(fc_macs, fc_bytes, int8_peak, hbm)
+    roof_sum_us = sum(roof_us) + fc_roof_us
+    mma_peak = None
+    if mma.get("int8_macs_per_clk_per_sm") and sm_mhz:
+        mma_peak = 2.0 * mma["int8_macs_per_clk_per_sm"] * mma.get("sm_count", 148) * sm_mhz * 1e6 / 1e12
+
+    # ---------------- weak scaling (N > 1): 256 images per GPU, same recipe
+    weak = None
+    if world > 1 and args.weak:
+        wmodel = resnet50_model(G)
+        wnet = GpuResNet50(wmodel, dev)
+        wnet.capture()
+        for _ in range(3):
+            wnet.replay()
+        wsteps = max(3, min(args.steps, 50))
+        wms = _time_replays(torch, wnet.replay, wsteps, world, dist, dev)
+        weak = {"value": round(G * world * wsteps / (wms / 1000.0), 1), "unit": "images/s",
+                "per_gpu_batch": G, "ms_per_step": round(wms / wsteps, 4), "steps": wsteps}
+        del wnet
 
     # ---------------- full network: the same convs plus max pool, 16 residual
     # qnn.add and global average pool between them; reported alongside, not as `value`
     full = None
     if args.full_network:
-        fm = resnet50_full_model(args.batch)
+        fm = shard_full_model(resnet50_full_model(G), lo, hi)
         fnet = GpuResNet50Full(fm, dev)
         fnet.capture()
         for _ in range(3):
             fnet.replay()
         torch.cuda.synchronize()
         fsteps = max(3, min(args.steps, 50))
-        if world > 1:
-            dist.barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for _ in range(fsteps):
-            fnet.replay()
-        f1.record()
-        torch.cuda.synchronize()
-        fms = max_over_ranks(f0.elapsed_time(f1), dist if world > 1 else None, dev) / fsteps
-        full = {"value": round(args.batch * world / (fms / 1000.0), 1), "unit": "images/s",
+        fms = _time_replays(torch, fnet.replay, fsteps, world, dist, dev) / fsteps
+        full = {"value": round(G / (fms / 1000.0), 1), "unit": "images/s",
                 "ms_per_step": round(fms, 4), "steps": fsteps, "launches_per_step": fnet.launches_per_step,
                 "ops": "quantize, conv1, max pool 3x3/2, 16 x (3-4 conv, the residual qnn.add + ReLU fused into "
                        "conv3's epilogue), global avg pool, fc, dequantize"}
@@ -623,32 +704,46 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(model, 1)
-    layers = [{"name": sp.name, "ms": round(float(t), 4), "tops": round(2.0 * m / (t / 1000.0) / 1e12, 1)}
-              for sp, t, m in zip(net.stack.specs, layer_ms, macs)]
+    layers = [{"name": sp.name, "ms": round(float(t), 4), "tops": round(2.0 * m / (t / 1000.0) / 1e12, 1),
+               "roof_us": round(r, 1), "frac_roofline": round(r / (t * 1000.0), 3)}
+              for sp, t, m, r in zip(net.stack.specs, layer_ms, macs, roof_us)]
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": args.batch * world, "per_gpu_batch": args.batch,
-                   "image": "224x224x3 f32 -> u8", "parallelism": f"dp{world} (batch shard, replicated weights, "
-                   "no data-path collective)", "weights": "s8 symmetric per-channel", "activations": "u8",
-                   "rounding": "UPWARD", "l2": "no flush: per-step working set (154 MB f32 input + ~1.9 GB "
-                   "activations) exceeds the 126 MB L2", "graph": "CUDA graph replay per step"},
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": G, "per_gpu_batch": batch,
+                   "image": "224x224x3 f32 -> u8", "parallelism": f"dp{world} (batch {G} sharded {G}/{world} per GPU, "
+                   "replicated weights, no data-path collective)", "weights": "s8 symmetric per-channel",
+                   "activations": "u8", "rounding": "UPWARD",
+                   "l2": "no flush: per-step working set (154 MB f32 input + ~1.9 GB activations at batch 256) "
+                         "exceeds the 126 MB L2", "graph": "CUDA graph replay per step"},
         "conv_tops": round(conv_tops, 1), "conv_pct_int8_peak": round(100 * conv_tops / int8_peak, 2),
         "e2e": {"value": round(e2e_value, 1), "unit": "images/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "note": "pinned f32 images H2D (copy stream, double-buffered: step k+1's copy overlaps step k) + graph + f32 logits D2H, every step"},
+                "note": "pinned f32 images H2D (copy stream, double-buffered: step k+1's copy overlaps step k) "
+                        "+ graph + f32 logits D2H, every step"},
         "gpu_launches": int(net.launches_per_step * args.steps),
-        "roofline": {"kernel": "tcgen05 GEMMs: qnn_gemm_i8_kernel + qnn_gemm_t_kernel (all 54 conv/fc launches of a step)", "bound": "tensor",
+        "roofline": {"kernel": "tcgen05 GEMMs: qnn_gemm_i8_kernel + qnn_gemm_t_kernel (all 54 conv/fc launches "
+                               "of a step)", "bound": "tensor",
                      "achieved": round(achieved, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
                      "frac": round(achieved / int8_peak, 4),
-                     "peak_note": "int8 dense = 2 x measured sustained bf16 (MEASURED_PEAKS.json) per the guide's "
-                                  "nominal 4.5/2.25 ratio",
+                     "peak_note": ("int8 dense = 2 x measured %s bf16 (MEASURED_PEAKS.json), the guide's nominal "
+                                   "4.5/2.25 ratio; %s because the timed region ran at %s MHz of %s") %
+                                  ("burst" if burst else "sustained", "burst" if burst else "sustained", sm_mhz, sm_max),
+                     "roofline_sum_frac": round(roof_sum_us / (gemm_ms * 1000.0), 4),
+                     "roofline_sum_us": round(roof_sum_us, 1),
+                     "roofline_sum_note": "sum over the 54 launches of max(ops / int8 peak, algorithmic bytes / "
+                                          "measured HBM) divided by the measured GEMM time of a step (SURVEY §8d C5)",
+                     "peak_mma_microbench": None if mma_peak is None else round(mma_peak, 1),
+                     "frac_mma_microbench": None if mma_peak is None else round(achieved / mma_peak, 4),
+                     "mma_note": "tools/micro/mma_rate.cu: tcgen05.mma kind::i8 M=128 N=256 issue rate "
+                                 "(profiles/mma_peak.json) x 148 SMs x the timed region's median SM clock",
                      "traffic": traffic, "launches_per_step": gemm_launches,
                      "kernel_share_of_step": round(gemm_ms / ms_per_step, 3),
                      "ops_per_step": gemm_ops},
         "clocks": clk,
         "cpu_baseline": cpu,
+        "weak_scaling": weak,
         "full_network": full,
         "layers": layers,
     }

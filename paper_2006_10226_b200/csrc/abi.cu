@@ -132,13 +132,17 @@ static bool derive_multiplier(double m, int32_t* M, int32_t* shift) {
   return true;
 }
 
-// multiplier -> (M, right shift) for the kernels; rsh >= 63 rounds every int32 product to 0
+// multiplier -> (M, right shift) for the kernels (reading R15).  Every product the kernels
+// round is |x * M| < 2^63 (x = an int32 accumulator, an 8-bit code minus its zero point, or an
+// int32 input minus its zero point, |x| <= 2^32 - 1; M < 2^31), so a right shift >= 64 rounds
+// it to 0 in both modes and is replaced by M = 0.  rsh = 63 is kept: with int32 input and
+// zp_in != 0, |x * M| reaches [2^62, 2^63) and rounds to +-1 (the 64-bit rq_round handles it).
 static bool kernel_multiplier(double m, int32_t* M, int32_t* rsh) {
   int32_t Mi, sh;
   if (!derive_multiplier(m, &Mi, &sh)) return false;
   const int r = 31 - sh;
   if (r < 1) return false;  // m >= 2^30: unsupported (reading R15)
-  if (r > 62) {
+  if (r > 63) {
     *M = 0;
     *rsh = 1;
   } else {
@@ -196,6 +200,12 @@ struct ConvPlan {
   int mode = 0;
   qnn_dtype_t out_dt = QNN_S32;
   // packed blob layout
+  // channel-major GEMM (gemm_t.cu) for wide pointwise layers: chosen at plan time (its weights
+  // are packed in the perm32 lane order as a second copy, pk_wt); at run time it also needs a
+  // 16-B aligned output, else the pixel-major kernel runs on pk_w
+  bool trans = false, t_wres = false;
+  int t_stages = 0, t_Kt = 0, t_bufs = 1;
+  size_t pk_wt = 0;
   size_t pk_w = 0, pk_off = 0, pk_off64 = 0, pk_dwtc_w = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
   // workspace layout
   size_t ws_pad = 0, ws_pixsum = 0, ws_rowsum = 0, ws_total = 0;
@@ -504,10 +514,44 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       }
     }
   }
+  {
+    // wide pointwise layers: the channel-major GEMM keeps each output channel's requantize
+    // constants in registers.  QNN_NO_TRANS=1 keeps the pixel-major kernel (A/B measurements);
+    // K_out = 64 runs as half a 128-channel block only with QNN_TRANS_MINK=64 (measured no
+    // faster than the pixel-major kernel on ResNet-50 layer1)
+    static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
+    static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
+    if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows && d->groups == 1 &&
+        d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
+        (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
+        pl.out_cs % 16 == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
+      const int num_kb = pl.nchunks;   // one tap
+      // preference: resident weights with a second output staging buffer per column group
+      // (>= 4 stages), then resident weights with one, then streamed weights
+      const int opts[3][2] = {{2, 1}, {1, 1}, {1, 0}};   // {buffers, weights resident}
+      for (const auto& o : opts) {
+        const int bufs = o[0];
+        const bool w_res = o[1] != 0;
+        const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res, bufs);
+        if (stages >= (bufs == 2 ? 4 : 3) && gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res, bufs) <= 226 * 1024) {
+          pl.trans = true;
+          pl.t_wres = w_res;
+          pl.t_stages = stages;
+          pl.t_bufs = bufs;
+          pl.t_Kt = round_up(d->K, 128);
+          break;
+        }
+      }
+    }
+  }
   const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
   off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
+  if (pl.trans) {
+    pl.pk_wt = off;
+    off = align256(off + (size_t)pl.t_Kt * pl.Cw);
+  }
   pl.pk_off = off;
   off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
   pl.pk_off64 = off;
@@ -598,6 +642,8 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
       e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R, d->S * d->C, pl.Cw, pl.Kpad, s);
     else
       e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
+    if (e == cudaSuccess && pl.trans)
+      e = launch_pack_weights(kernel, pk + pl.pk_wt, d->K, 1, d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
                             pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off),
@@ -778,36 +824,27 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     }
   }
 
-  // wide pointwise layers: the channel-major GEMM (gemm_t.cu) keeps each output channel's
-  // requantize constants in its TMEM lane's registers.  QNN_NO_TRANS=1 keeps the pixel-major
-  // kernel (A/B measurements).
-  static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
-  // (K_out = 64 runs as half a 128-channel block: measured no faster than the pixel-major
-  // kernel on ResNet-50 layer1, so off unless QNN_TRANS_MINK=64)
-  static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
-  if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows &&
-      d->groups == 1 && d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
-      (pl.out_dt == DT_U8 || pl.out_dt == DT_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
-      pl.out_cs % 16 == 0 &&
-      (reinterpret_cast<uintptr_t>(output) & 15) == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
+  // wide pointwise layers (plan: pl.trans): the channel-major GEMM (gemm_t.cu) on the perm32 weights
+  if (pl.trans && (reinterpret_cast<uintptr_t>(output) & 15) == 0) {
     const int num_kb = pl.nchunks;   // one tap
-    bool w_res = gemm_t_max_stages(pl.BK, num_kb, true) >= 3 &&
-                 gemm_t_smem_bytes(pl.BK, num_kb, gemm_t_max_stages(pl.BK, num_kb, true), true) <= 226 * 1024;
-    const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res);
-    if (stages >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res) <= 226 * 1024) {
+    const bool w_res = pl.t_wres;
+    const int stages = pl.t_stages;
+    {
       alignas(64) CUtensorMap tmX, tmW, tmC, tmR;
       std::memset(&tmR, 0, sizeof(tmR));
       const int a_chan = d->C;
-      bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, 256) &&
-                 encode_2d(&tmW, pk + pl.pk_w, (uint64_t)pl.Cw, (uint64_t)pl.Kpad, (uint64_t)pl.Cw, pl.BK, 128) &&
-                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 32, 64, false) &&
-                 (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, 32, 64, false));
+      bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmTBN) &&
+                 encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)pl.Cw, (uint64_t)pl.t_Kt, (uint64_t)pl.Cw, pl.BK, 128) &&
+                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 128, kGemmTBN / 4) &&
+                 (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, 128,
+                                    kGemmTBN / 4));
       if (okt) {
         GemmTParams tp{};
         tp.BK = pl.BK;
         tp.stages = stages;
         tp.num_kb = num_kb;
         tp.w_res = w_res;
+        tp.stage_bufs = pl.t_bufs;
         tp.num_ch_tiles = (d->K + 127) / 128;
         tp.Kout = d->K;
         if (res) {
@@ -817,18 +854,20 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
           tp.res_zp = res->zp;
           tp.res_s8 = res->dtype == QNN_S8;
         }
-        tp.num_px_tiles = (int)((pl.M + 255) / 256);
-        tp.idesc = make_idesc_i8(1, a_signed, 128, 256);   // A = s8 weights, B = activations
+        tp.num_px_tiles = (int)((pl.M + kGemmTBN - 1) / kGemmTBN);
+        tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights, B = activations
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
         tp.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
         tp.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
         tp.zp_out = pl.zp_out;
         tp.lo = pl.lo;
         tp.hi = pl.hi;
+#ifdef QNN_GEMM_INSTRUMENT
         {
           static const char* dbg_env = std::getenv("QNN_GEMM_DEBUG");
           tp.dbg = dbg_env ? std::atoi(dbg_env) : 0;
         }
+#endif
         const int sms = sm_count();
         const int tiles = tp.num_ch_tiles * tp.num_px_tiles;
         const int grid = tiles <= sms ? tiles : std::max(1, sms / tp.num_ch_tiles) * tp.num_ch_tiles;

@@ -35,6 +35,18 @@ __device__ __forceinline__ int64_t rq_round(int64_t p, int rsh, int mode) {
   }
 }
 
+// hi32(x * M + K) for int32 x, M and a 64-bit K: this exact PTX shape (mul.wide + add.s64 +
+// high half) is what ptxas turns into ONE IMAD.HI with K as its 64-bit addend; a mad.wide.s32
+// became IMAD.WIDE + IADD3 + IMAD.X, and plain 64-bit C++ sometimes a full 64x64 multiply
+__device__ __forceinline__ int32_t mad_hi64(int32_t x, int32_t M, long long K) {
+  int32_t h;
+  asm("{\n\t.reg .s64 p;\n\t.reg .b32 lo;\n\t"
+      "mul.wide.s32 p, %1, %2;\n\tadd.s64 p, p, %3;\n\tmov.b64 {lo, %0}, p;\n\t}"
+      : "=r"(h)
+      : "r"(x), "r"(M), "l"(K));
+  return h;
+}
+
 // Requantize an exact int64 value and apply zp_out + clamp [lo, hi] (already
 // intersected with the dtype range and the ReLU bound on the host).
 __device__ __forceinline__ int32_t rq_apply(int64_t v, int32_t M, int rsh, int mode, int32_t zp, int32_t lo,

@@ -277,9 +277,7 @@ __device__ __forceinline__ void dw3_items(const DwParams& p, int c0, int first, 
           for (int ch = 0; ch < 4; ++ch) {
             int32_t v;
             if (FAST) {
-              const unsigned long long pr =
-                  (unsigned long long)((long long)acc[op][q][ch] * Mc[ch]) + (unsigned long long)Kc[ch];
-              v = (int32_t)(pr >> 32) >> Tc[ch];
+              v = mad_hi64(acc[op][q][ch], Mc[ch], Kc[ch]) >> Tc[ch];
             } else {
               const int32_t xv = (int32_t)((uint32_t)acc[op][q][ch] + (uint32_t)off32[ch]);
               v = rq_apply(xv, Mc[ch], Rc[ch], p.mode, p.zp_out, p.lo, p.hi);

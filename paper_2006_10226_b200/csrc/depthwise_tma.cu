@@ -78,7 +78,10 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
   for (int it = threadIdx.x; it < items; it += kDwtThreads) {
     const int q = it >> lg;   // (it % G == g: kDwtThreads % G == 0)
     const int x = q * SH;     // box column of the first tap (box starts at input column -pl)
-    const bool c0ok = x - pl >= 0, c2ok = x + 2 - pl < Wd;   // the middle tap is always inside
+    // every tap's column checked against [0, W): with pl >= 2 (or a right pad >= 2) the middle
+    // tap can fall outside the image too, and the TMA zero fill is not zp_A
+    const bool c0ok = (unsigned)(x - pl) < (unsigned)Wd, c1ok = (unsigned)(x + 1 - pl) < (unsigned)Wd,
+               c2ok = (unsigned)(x + 2 - pl) < (unsigned)Wd;
     uint32_t a = st_base + (uint32_t)(x * cs);
     uint8_t* dst = out + (long long)q * p.out_cstride;
     uint32_t T0[4], T1[4], T2[4];   // per-channel words of the last three input rows (bytes: 3 taps + junk)
@@ -94,7 +97,7 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[1]) : "r"(a + cs));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[2]) : "r"(a + 2 * cs));
       wv[0] = row_ok && c0ok ? wv[0] : zfill;
-      wv[1] = row_ok ? wv[1] : zfill;
+      wv[1] = row_ok && c1ok ? wv[1] : zfill;
       wv[2] = row_ok && c2ok ? wv[2] : zfill;
       // 3 pixels x 4 channels -> 4 channels x 3 pixels (byte 3 multiplies the filter's 0)
       const uint32_t t0 = __byte_perm(wv[0], wv[1], 0x5140), t1 = __byte_perm(wv[0], wv[1], 0x7362);
@@ -116,8 +119,7 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
         acc = dwt_dp4a<ASIGNED>(T2[ch], wr[2][ch], acc);
         int32_t v;
         if (FAST) {
-          const unsigned long long pr = (unsigned long long)((long long)acc * Mc[ch]) + (unsigned long long)Kc[ch];
-          v = (int32_t)(pr >> 32) >> Tc[ch];
+          v = mad_hi64(acc, Mc[ch], Kc[ch]) >> Tc[ch];
         } else {
           const int32_t xv = (int32_t)((uint32_t)acc + (uint32_t)off32[ch]);
           v = rq_apply(xv, Mc[ch], Rc[ch], p.mode, p.zp_out, p.lo, p.hi);

@@ -90,6 +90,10 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ void bulk_wait_read_dyn(int n) {   // n in {0, 1}
+  if (n) bulk_wait_read<1>();
+  else bulk_wait_read<0>();
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -185,10 +189,8 @@ __device__ __forceinline__ void epi_chunk_up(const uint32_t (&v)[32], const int4
         v0 -= rterm;
         v1 -= rterm;
       }
-      const unsigned long long p0 = (unsigned long long)((long long)v0 * mt.x) + (unsigned long long)kk.x;
-      const unsigned long long p1 = (unsigned long long)((long long)v1 * mt.z) + (unsigned long long)kk.y;
-      int32_t r0 = (int32_t)(p0 >> 32) >> mt.y;
-      int32_t r1 = (int32_t)(p1 >> 32) >> mt.w;
+      int32_t r0 = mad_hi64(v0, mt.x, kk.x) >> mt.y;   // one IMAD.HI with the 64-bit K as addend
+      int32_t r1 = mad_hi64(v1, mt.z, kk.y) >> mt.w;
       if (RES) {
         r0 += res_val(*rt, rw[q4], 2 * h);
         r1 += res_val(*rt, rw[q4], 2 * h + 1);

@@ -8,15 +8,19 @@
 // are bound by that epilogue.  Here the MMA computes D^T = W * A^T: M = 128 output channels
 // (A operand = the packed weights, resident in shared memory for the CTA's channel block),
 // N = 256 pixels (B operand = the activation rows, streamed by TMA), so a TMEM lane is ONE
-// output channel and its multiplier / shift / 64-bit constant live in that lane's registers
-// for the whole kernel.  Bytes go to a [64 pixels][32 channels] staging tile with one STS.U8
-// each and leave by TMA store.
+// output channel.  The weight rows are packed in the order perm32 (prep.cu): TMEM lane
+// j + 8i of a 32-lane quadrant holds channel 4j + i, so the 16x256b TMEM load (thread
+// (j = lane/4, u = lane%4) receives lanes j and j+8, or j+16 and j+24, at pixel columns
+// 8r + 2u + {0, 1}) hands every thread four CONSECUTIVE output channels of a pixel: their
+// four requantize constants live in its registers for the whole kernel, and each requantized
+// group of four is one packed 32-bit word, stored with one STS.32 into a [64 pixels][32
+// channels] staging tile that leaves by TMA store (previously one STS.U8 per output byte).
 //
 // Grid: a multiple of the channel-block count, so a CTA keeps one channel block (weights and
 // constants loaded once; weights streamed per stage when the block does not fit); pixel
 // tiles advance by grid / blocks.
-// Warps: 0-15 epilogue (warp w: TMEM lanes 32*(w%4) = its 32 channels, pixel columns
-// 64*(w/4)), 16 TMA producer, 17 MMA issuer + TMEM allocator (2 accumulators x 256 columns).
+// Warps: 0-15 epilogue (warp w: TMEM lanes 32*(w%4), pixel columns 64*(w/4)), 16 TMA
+// producer, 17 MMA issuer + TMEM allocator (2 accumulators x 256 columns).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -36,52 +40,115 @@ namespace qnn {
 
 namespace {
 
+#ifdef QNN_GEMM_INSTRUMENT
+constexpr bool kTInstrument = true;    // QNN_GEMM_DEBUG knobs compiled in (profiling builds only)
+#else
+constexpr bool kTInstrument = false;
+#endif
+
 constexpr int kTEpiWarps = 16;
 constexpr int kTThreads = 32 * kTEpiWarps + 64;
 constexpr int kTBM = 128;   // output channels per tile (MMA M)
-constexpr int kTBN = 256;   // pixels per tile (MMA N)
-constexpr int kTStageOut = 2048;   // per epilogue warp: 64 pixels x 32 channels
+constexpr int kTBN = kGemmTBN;          // pixels per tile (MMA N), internal.h
+constexpr int kTNacc = 512 / kTBN;      // TMEM accumulator buffers (512 columns)
+constexpr int kTCols = kTBN / 4;        // pixel columns per epilogue warp (4 column groups)
+constexpr int kTHalves = kTCols / 32;   // 32-column steps per warp and tile
+// output staging, per column group (the 4 warps of one group of pixel columns share it):
+// [kTCols pixels][128 channels] in the TMA 128-B swizzle (16-B chunk c of row r at chunk
+// c ^ (r % 8)), one TMA store of 128-B rows per group and tile; 1 or 2 buffers (host choice)
+constexpr int kTGroupOut = kTCols * 128;
+#ifdef QNN_T_SPIN
+#define QNN_T_WAIT mbar_wait_spin
+#else
+#define QNN_T_WAIT mbar_wait
+#endif
 
-__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
-
-// two outputs of one channel (pixels j, j+1): clamp, saturate, one byte each into the
-// [pixel][channel] staging tile
-template <bool CLAMP, bool S8OUT>
-__device__ __forceinline__ void store2(uint32_t a, int32_t y0, int32_t y1, int32_t lo, int32_t hi) {
-  if (CLAMP) {
-    y0 = min(max(y0, lo), hi);
-    y1 = min(max(y1, lo), hi);
-  }
-  uint32_t b2;   // saturated bytes (y0, y1) in the low half-word
-  if (S8OUT)
-    asm("cvt.pack.sat.s8.s32.b32 %0, %2, %1, 0;" : "=r"(b2) : "r"(y0), "r"(y1));
-  else
-    asm("cvt.pack.sat.u8.s32.b32 %0, %2, %1, 0;" : "=r"(b2) : "r"(y0), "r"(y1));
-  sts_u8(a, b2);
-  sts_u8(a + 32, b2 >> 8);
-}
-
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
+}
+
+// 16 TMEM lanes x 32 columns (16x256b.x4), not waited: thread (j, u) = (lane/4, lane%4)
+// receives r[4k + e] = (lane base + j, column 8k + 2u + e), r[4k + 2 + e] = (base + 8 + j, same)
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16x2(uint32_t (&a)[16], uint32_t (&b)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]),
+                 "+r"(a[15]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]),
+                 "+r"(b[7]), "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]),
+                 "+r"(b[14]), "+r"(b[15])
+               :
+               : "memory");
 }
 
 // the residual byte requantized to the output scale with zero point 0 (reading R19: added
 // to the conv's requantized value before the clamp)
 template <int MODE>
-__device__ __forceinline__ int32_t res_term(const GemmTParams& p, uint32_t b) {
+__device__ __forceinline__ int32_t res_term(const GemmTParams& p, uint32_t word, int byte) {
+  const uint32_t b = (word >> (8 * byte)) & 0xFFu;
   const int32_t x = (p.res_s8 ? (int32_t)(int8_t)b : (int32_t)b) - p.res_zp;
   return (int32_t)rq_round((int64_t)x * p.res_M, p.res_rsh, MODE);
 }
 
-// hi32(v * M + K) (64-bit addend): one IMAD.WIDE
-__device__ __forceinline__ int32_t madwide_hi(int32_t v, int32_t M, long long K) {
-  long long d;
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(v), "r"(M), "l"(K));
-  return (int32_t)((unsigned long long)d >> 32);
+// one thread's four channels: requantize constants in registers for the whole kernel
+//   fast (UPWARD, rsh = 32 + t, t in [1, 20]): y = hi32(v * M + K) >> t with the 64-bit
+//     K = off * M + (2^(t-1) + zp_out * 2^t) * 2^32 (modular int64: exact whenever the true
+//     v + off fits int32, reading R10).  Written as 64-bit C++ so ptxas emits ONE IMAD.HI with
+//     the persistent 64-bit K as its addend (an inline mad.wide became IMAD.WIDE + IMAD.X).
+//   generic: exact 64-bit rounding of (v + off) * M by rsh (k holds off, t holds rsh)
+struct TChan {
+  int32_t M[4], t[4];
+  long long k[4];
+};
+
+template <int MODE, bool FAST>
+__device__ __forceinline__ int32_t tq1(const TChan& q, int i, uint32_t acc, int32_t zp_out) {
+  if (FAST) return mad_hi64((int32_t)acc, q.M[i], q.k[i]) >> q.t[i];
+  const long long z = rq_round(((long long)(int32_t)acc + q.k[i]) * q.M[i], q.t[i], MODE) + zp_out;
+  return (int32_t)(z < INT32_MIN ? INT32_MIN : (z > INT32_MAX ? INT32_MAX : z));
+}
+
+// 32 of the warp's pixel columns x its quadrant's 32 channels: requantize, (residual), clamp,
+// pack 4 channels per word, store into the staging tile [pixel][32 channels]
+template <int MODE, bool FAST, bool CLAMP, bool S8OUT, bool RES>
+__device__ __forceinline__ void t_epilogue(const GemmTParams& p, const TChan& q, const uint32_t (&va)[16],
+                                           const uint32_t (&vb)[16], uint32_t st0, uint32_t st1) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      // pixel column 8k + 2u + e of this 32-column step; channels 4j + i from lanes j, j+8 (va)
+      // and j+16, j+24 (vb); the swizzled word address depends on e and the thread only
+      const uint32_t a = (e ? st1 : st0) + (uint32_t)(8 * k * 128);
+      int32_t y[4];
+      y[0] = tq1<MODE, FAST>(q, 0, va[4 * k + e], p.zp_out);
+      y[1] = tq1<MODE, FAST>(q, 1, va[4 * k + 2 + e], p.zp_out);
+      y[2] = tq1<MODE, FAST>(q, 2, vb[4 * k + e], p.zp_out);
+      y[3] = tq1<MODE, FAST>(q, 3, vb[4 * k + 2 + e], p.zp_out);
+      if (RES) {
+        const uint32_t rw = lds32(a);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) y[i] += res_term<MODE>(p, rw, i);
+      }
+      if (CLAMP || !FAST) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) y[i] = min(max(y[i], p.lo), p.hi);
+      }
+      sts32(a, S8OUT ? pack4_s8(y[0], y[1], y[2], y[3]) : pack4_u8(y[0], y[1], y[2], y[3]));
+    }
+  }
 }
 
 }  // namespace
@@ -90,15 +157,15 @@ constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers a
 
 // w_res: the CTA's weight block stays resident (num_kb blocks); otherwise each pipeline stage
 // carries its weight k-block next to the activation k-block
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res) {
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs) {
   const size_t stage = (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK);
   return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK : 0) +
-         (size_t)kTEpiWarps * kTStageOut + 256;
+         (size_t)4 * kTGroupOut * stage_bufs + 256;
 }
 
-int gemm_t_max_stages(int BK, int num_kb, bool w_res) {
-  int s = 6;
-  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s, w_res) > (size_t)kTSmemMax) --s;
+int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs) {
+  int s = 8;
+  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs) > (size_t)kTSmemMax) --s;
   return s;
 }
 
@@ -115,7 +182,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint8_t* sX = smem;                                  // stages x [256 pixels][BK]
   uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb (resident) or stages x [128 channels][BK]
   uint8_t* sOut = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // 16 x [64 pixels][32 channels]
-  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2], wfull, rbar[kTEpiWarps];
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[4];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = kTEpiWarps, kMmaWarp = kTEpiWarps + 1;
@@ -131,12 +198,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kTNacc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kTEpiWarps);
     }
     mbar_init(&wfull, 1);
-    for (int w = 0; w < kTEpiWarps; ++w) mbar_init(&rbar[w], 1);
+    for (int g = 0; g < 4; ++g) mbar_init(&rbar[g], 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(&tmem_slot, 512);
@@ -155,7 +222,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     uint32_t phase = 0;
     for (int pt = px_first; pt < npt; pt += px_step) {
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        QNN_T_WAIT(&empty[stage], phase ^ 1);
         if (leader) {
           mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes));
           tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
@@ -177,12 +244,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
     uint32_t phase = 0;
     if (w_res && px_first < npt) mbar_wait(&wfull, 0);
     for (int pt = px_first; pt < npt; pt += px_step, ++it) {
-      const int acc = it & 1;
-      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      const int acc = it % kTNacc;
+      QNN_T_WAIT(&tempty[acc], ((it / kTNacc) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)acc * kTBN;
       for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        QNN_T_WAIT(&full[stage], phase);
         tc_fence_after();
         if (leader) {
           const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage) * w16, xd = xdesc0 + (uint64_t)stage * x16;
@@ -201,133 +268,90 @@ __global__ void __launch_bounds__(kTThreads, 1)
   } else if (warp < kTEpiWarps) {
     // ---------------------------------------------------------------- epilogue
     const int quad = warp & 3, grp = warp >> 2;
-    const int k = ch * kTBM + quad * 32 + lane;   // this lane's output channel
-    // (K_out = 64: the upper half of the 128-channel block is zero weights; its lanes compute
+    const int j = lane >> 2, u = lane & 3;
+    // (K_out = 64: the upper half of the 128-channel block is zero weights; its quads compute
     // nothing and their stores fall outside the output tensor, which TMA drops)
     const bool quad_live = ch * kTBM + quad * 32 < p.Kout;
-    const int kk = k < p.Kout ? k : 0;
-    const int32_t M = p.mult[kk], rsh = p.rsh[kk];
-    const long long off = p.off64[kk];
-    const bool fast = MODE == 0 && rsh >= 33 && rsh <= 52;
-    int t = 0;
-    long long K = 0;
-    if (fast) {
-      t = rsh - 32;
-      const unsigned long long c64 = (1ull << (t - 1)) + ((unsigned long long)(long long)p.zp_out << t);
-      K = (long long)((unsigned long long)off * (unsigned long long)(long long)M + (c64 << 32));
+    TChan q;
+    bool fast = MODE == 0;
+    const int k0 = ch * kTBM + quad * 32 + 4 * j;   // this thread's channels k0 .. k0 + 3
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = k0 + i < p.Kout ? k0 + i : 0;
+      const int32_t rsh = p.rsh[kk];
+      const long long off = p.off64[kk];
+      q.M[i] = p.mult[kk];
+      if (MODE == 0 && rsh >= 33 && rsh <= 52) {
+        const int t = rsh - 32;
+        const unsigned long long c64 = (1ull << (t - 1)) + ((unsigned long long)(long long)p.zp_out << t);
+        q.t[i] = t;
+        q.k[i] = (long long)((unsigned long long)off * (unsigned long long)(long long)q.M[i] + (c64 << 32));
+      } else {
+        fast = false;
+        q.t[i] = rsh;
+        q.k[i] = off;
+      }
     }
+    const int dbg = kTInstrument ? p.dbg : 0;
     const bool all_fast = __all_sync(0xffffffffu, fast);
-    // 32-bit form of the fast path: with |acc| <= KK * 255 * 255 (any operand dtypes / zps) and
-    // |off| below 2^31 minus that bound, acc + off is exact in int32, and since the rounding
-    // constant c64 has no bits below 2^32,  hi64((acc + off) * M + c64 * 2^32) = hi32((acc + off) * M) + c64:
-    // one IMAD.HI with a 32-bit addend instead of a 64-bit multiply-add with carry.
-    const long long acc_bound = (long long)p.num_kb * p.BK * 65025LL;
-    const bool fast32 = fast && (off < 0 ? -off : off) < (1LL << 31) - 1 - acc_bound;
-    const int32_t off32 = (int32_t)off;
-    const int32_t c32 = fast ? (int32_t)((1 << (t - 1)) + p.zp_out * (1 << t)) : 0;
-    const bool all_fast32 = __all_sync(0xffffffffu, fast32) && !(p.dbg & 4);
-    uint8_t* stage_out = sOut + warp * kTStageOut;
-    const uint32_t st_lane = smem_u32(stage_out) + (uint32_t)lane;
+    // column group grp shares a [kTCols][128] staging tile (1 or 2 buffers) with the other 3
+    // quads; its quad-0 lane 0 issues the group's TMA store (and residual load)
+    const bool gleader = quad == 0 && lane == 0;
+    const int nbufs = p.stage_bufs;
+    uint8_t* const gstage = sOut + (size_t)grp * kTGroupOut * nbufs;
+    // this thread's words (pixel rows 2u + e, e = 0/1; channel word 8 quad + j) in the 128-B swizzle
+    const uint32_t ch16 = (uint32_t)(2 * quad + (j >> 2));
+    const uint32_t st_off0 = (uint32_t)(2 * u) * 128 + ((ch16 ^ (uint32_t)(2 * u)) << 4) + (uint32_t)((j & 3) << 2);
+    const uint32_t st_off1 = (uint32_t)(2 * u + 1) * 128 + ((ch16 ^ (uint32_t)(2 * u + 1)) << 4) +
+                             (uint32_t)((j & 3) << 2);
     int it = 0;
     for (int pt = px_first; pt < npt; pt += px_step, ++it) {
-      const int acc = it & 1;
-      if (RES) {
-        // the residual tile (this warp's 64 pixels x 32 channels) lands in the staging tile
-        // itself; each lane then reads its channel's byte per pixel and overwrites it
-        if (lane == 0) {
-          bulk_wait_read<0>();   // the previous tile's store has read the staging tile
-          if (quad_live) {
-            mbar_arrive_expect_tx(&rbar[warp], kTStageOut);
-            tma_load_2d(stage_out, &tmR, &rbar[warp], ch * kTBM + quad * 32, pt * kTBN + grp * 64);
-          }
+      const int acc = it % kTNacc;
+      uint8_t* const stage_out = gstage + (nbufs == 2 ? (it & 1) * kTGroupOut : 0);
+      const uint32_t sbase = smem_u32(stage_out);
+      if (gleader) {
+        bulk_wait_read_dyn(nbufs - 1);   // the store that last used this buffer has read it
+        if (RES) {
+          // the residual tile (this group's pixels x 128 channels, same swizzle) lands in the
+          // staging buffer; each thread reads its four channels' word per pixel and overwrites it
+          mbar_arrive_expect_tx(&rbar[grp], kTGroupOut);
+          tma_load_2d(stage_out, &tmR, &rbar[grp], ch * kTBM, pt * kTBN + grp * kTCols);
         }
-        __syncwarp();
       }
-      QNN_EPI_WAIT(&tfull[acc], (it >> 1) & 1);
+      named_bar_sync(1 + grp, 128);      // the buffer is free for every warp of the group
+      QNN_EPI_WAIT(&tfull[acc], (it / kTNacc) & 1);
       tc_fence_after();
-      const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 64);
-      uint32_t va[32], vb[32];
-      tmem_ld32_nowait(tb, va);
-      tmem_ld32_nowait(tb + 32, vb);
-      tmem_wait32(va);
-      tmem_wait32(vb);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&tempty[acc]);
-        if (!RES) bulk_wait_read<0>();   // the previous tile's store has read the staging tile
-      }
-      __syncwarp();
-      if (RES && quad_live) mbar_wait(&rbar[warp], (uint32_t)(it & 1));
-      // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
-      if ((p.dbg & 1) || !quad_live) {
-      } else if (all_fast32) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t* v = h ? vb : va;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
-            int32_t y0 = __mulhi((int32_t)v[j] + off32, M) + c32, y1 = __mulhi((int32_t)v[j + 1] + off32, M) + c32;
-            y0 >>= t;
-            y1 >>= t;
-            if (RES) {
-              y0 += res_term<MODE>(p, lds_u8(a));
-              y1 += res_term<MODE>(p, lds_u8(a + 32));
-            }
-            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
-          }
+      const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * kTCols);
+      if (RES) mbar_wait(&rbar[grp], (uint32_t)(it & 1));
+      // steps of 32 pixel columns (register budget: 96 per thread at 18 warps)
+#pragma unroll 1
+      for (int h = 0; h < kTHalves; ++h) {
+        uint32_t va[16], vb[16];
+        tmem_ld_16x256b_x4(tb + 32 * h, va);                  // lanes j, j + 8
+        tmem_ld_16x256b_x4(tb + 32 * h + (16u << 16), vb);    // lanes j + 16, j + 24
+        tmem_wait16x2(va, vb);
+        if (h == kTHalves - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-      } else if (all_fast) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t* v = h ? vb : va;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
-            int32_t y0 = madwide_hi((int32_t)v[j], M, K) >> t, y1 = madwide_hi((int32_t)v[j + 1], M, K) >> t;
-            if (RES) {
-              y0 += res_term<MODE>(p, lds_u8(a));
-              y1 += res_term<MODE>(p, lds_u8(a + 32));
-            }
-            store2<CLAMP, S8OUT>(a, y0, y1, p.lo, p.hi);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t* v = h ? vb : va;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const uint32_t a = st_lane + (uint32_t)((h * 32 + j) * 32);
-            int64_t z0, z1;   // exact: requantized value + zp_out (+ residual), clamped below
-            if (fast) {
-              z0 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j] * M) + (unsigned long long)K) >> 32) >> t;
-              z1 = (int32_t)(((unsigned long long)((long long)(int32_t)v[j + 1] * M) + (unsigned long long)K) >> 32) >>
-                   t;
-            } else {
-              z0 = rq_round(((long long)(int32_t)v[j] + off) * M, rsh, MODE) + p.zp_out;
-              z1 = rq_round(((long long)(int32_t)v[j + 1] + off) * M, rsh, MODE) + p.zp_out;
-            }
-            if (RES) {
-              z0 += res_term<MODE>(p, lds_u8(a));
-              z1 += res_term<MODE>(p, lds_u8(a + 32));
-            }
-            const int32_t y0 = (int32_t)(z0 < p.lo ? p.lo : (z0 > p.hi ? p.hi : z0));
-            const int32_t y1 = (int32_t)(z1 < p.lo ? p.lo : (z1 > p.hi ? p.hi : z1));
-            store2<false, S8OUT>(a, y0, y1, p.lo, p.hi);
-          }
+        const uint32_t rowb = sbase + (uint32_t)(h * 32 * 128);
+        // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
+        if ((dbg & 1) || !quad_live) {
+        } else if (all_fast) {
+          t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va, vb, rowb + st_off0, rowb + st_off1);
+        } else {
+          t_epilogue<MODE, false, CLAMP, S8OUT, RES>(p, q, va, vb, rowb + st_off0, rowb + st_off1);
         }
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0 && quad_live && !(p.dbg & 2)) {
-        tma_store_2d(&tmC, stage_out, ch * kTBM + quad * 32, pt * kTBN + grp * 64);
+      named_bar_sync(1 + grp, 128);      // every warp of the group has written its channels
+      if (gleader && !(dbg & 2)) {
+        tma_store_2d(&tmC, stage_out, ch * kTBM, pt * kTBN + grp * kTCols);
         bulk_commit();
       }
-      __syncwarp();
     }
-    if (lane == 0) bulk_wait_all();
+    if (gleader) bulk_wait_all();
     __syncwarp();
   }
   tc_fence_before();
@@ -342,16 +366,18 @@ cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream) {
   const bool res = p.has_res;
-  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res);
+  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res, p.stage_bufs);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
+  int dev = 0;
+  cudaGetDevice(&dev);
 #define QNN_GT(M_, C_, S_, R_)                                                                             \
   if (mode == M_ && clamp == C_ && s8out == S_ && res == R_) {                                             \
     auto kern = qnn_gemm_t_kernel<M_, C_, S_, R_>;                                                         \
-    static bool attr = false;                                                                              \
-    if (!attr) {                                                                                           \
+    static int attr_done[64] = {0};   /* per device: a process may drive several GPUs */                  \
+    if (dev >= 64 || !attr_done[dev]) {                                                                    \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmemMax);  \
       if (e != cudaSuccess) return e;                                                                      \
-      attr = true;                                                                                         \
+      if (dev < 64) attr_done[dev] = 1;                                                                    \
     }                                                                                                      \
     kern<<<grid, kTThreads, smem, stream>>>(tmX, tmW, tmC, tmR, p);                                        \
     count_launch();                                                                                        \

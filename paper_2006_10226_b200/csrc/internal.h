@@ -64,6 +64,10 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
 
 // Channel-major GEMM (gemm_t.cu): wide 1x1 convs, D^T = W * A^T with the output channels on
 // the TMEM lanes (per-lane requantize constants in registers).
+#ifndef QNN_T_BN
+#define QNN_T_BN 256
+#endif
+constexpr int kGemmTBN = QNN_T_BN;   // pixels per channel-major tile (MMA N; 128 or 256)
 struct GemmTParams {
   int BK, stages, num_kb, num_ch_tiles, num_px_tiles;
   int w_res;             // weight block resident (else streamed per stage)
@@ -75,10 +79,11 @@ struct GemmTParams {
   const int32_t* rsh;    // [Kpad]
   const int64_t* off64;  // [Kpad] (single border class)
   int32_t zp_out, lo, hi;
-  int dbg;   // QNN_GEMM_DEBUG (profiling): 1 skips the epilogue math, 2 the TMA stores
+  int stage_bufs;         // output staging buffers per column group (1 or 2)
+  int dbg;   // QNN_GEMM_DEBUG (instrumented builds only): 1 skips the epilogue math, 2 the TMA stores
 };
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res);
-int gemm_t_max_stages(int BK, int num_kb, bool w_res);
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs);
+int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream);
@@ -166,7 +171,7 @@ struct ClassTable {
 };
 
 cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad,
-                                cudaStream_t s);
+                                cudaStream_t s, int perm32 = 0);
 cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
                                 int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int64_t* off64, int Kpad,
                                 cudaStream_t s);

@@ -19,26 +19,31 @@
 
 namespace qnn {
 
+// perm32: row r of every 32-row group holds channel 4*(r % 8) + (r / 8) % 4 of that group -- the
+// TMEM lane order of the channel-major GEMM (gemm_t.cu), whose 16x256b TMEM loads then hand a
+// thread four consecutive output channels of one pixel
 __global__ void pack_weights_kernel(const uint8_t* __restrict__ W, uint8_t* __restrict__ Wp, int K, int RS, int C,
-                                    int Cw, int Kpad) {
+                                    int Cw, int Kpad, int perm32) {
   const long long total = (long long)Kpad * RS * Cw;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cw);
     const long long t = i / Cw;
     const int tap = (int)(t % RS);
-    const int k = (int)(t / RS);
+    const int row = (int)(t / RS);
+    const int k = perm32 ? (row & ~31) | (4 * (row & 7) + ((row >> 3) & 3)) : row;
     uint8_t v = 0;
     if (k < K && c < C) v = W[((long long)k * RS + tap) * C + c];
     Wp[i] = v;
   }
 }
 
-cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad, cudaStream_t s) {
+cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad, cudaStream_t s,
+                                int perm32) {
   const long long total = (long long)Kpad * RS * Cw;
   const int threads = 256;
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 4096);
-  pack_weights_kernel<<<blocks, threads, 0, s>>>((const uint8_t*)W, (uint8_t*)Wp, K, RS, C, Cw, Kpad);
+  pack_weights_kernel<<<blocks, threads, 0, s>>>((const uint8_t*)W, (uint8_t*)Wp, K, RS, C, Cw, Kpad, perm32);
   count_launch();
   return cudaGetLastError();
 }

@@ -79,3 +79,42 @@ def mismatch_report(got: np.ndarray, want: np.ndarray, limit: int = 8) -> str:
         b = tuple(b)
         lines.append(f"  at {b}: got {got[b]} want {want[b]}")
     return "\n".join(lines)
+
+
+def ref_conv_lib(A_nhwc, W_ohwi, zp_A, zp_W, bias, s_A, s_W, out, stride=(1, 1), pad=(0, 0, 0, 0), dil=(1, 1),
+                 groups=1, chunk=16):
+    """Exact reference for FULL-SIZE layers (too large for the int64 loop oracle in a test).
+
+    Eq. 2's integer core sum (a - zp_A)(w - zp_W) through a library routine, torch float64
+    conv2d on the zero-point-subtracted operands (zero padding of a - zp_A == zp_A padding of
+    a): every product and partial sum is an integer below 255^2 * 4608 < 2^53, so the
+    float64 result is exact in any summation order (SURVEY §8c pins: "Term 1 / zp = 0 special
+    case ... torch.nn.functional.conv2d in float64 is exact here").  Bias and the requantize
+    (Eq. 5) are the oracle's own exact-rational routines.  Returns NHWC."""
+    import torch.nn.functional as F
+    N = A_nhwc.shape[0]
+    K = W_ohwi.shape[0]
+    Wd = torch.from_numpy(np.ascontiguousarray(W_ohwi.transpose(0, 3, 1, 2)).astype(np.float64) - zp_W)
+    b = np.zeros(K, np.int64) if bias is None else np.asarray(bias, np.int64)
+    if out is not None:
+        M, S = orc.conv_multipliers(s_A, s_W, out["scale"], K)
+    res = []
+    for n0 in range(0, N, chunk):
+        a = torch.from_numpy(np.ascontiguousarray(A_nhwc[n0:n0 + chunk].transpose(0, 3, 1, 2)).astype(np.float64)
+                             - zp_A)
+        a = F.pad(a, (pad[1], pad[3], pad[0], pad[2]))
+        acc = F.conv2d(a, Wd, stride=tuple(stride), dilation=tuple(dil), groups=groups)
+        acc = acc.numpy().astype(np.int64) + b[None, :, None, None]
+        if out is None:
+            y = acc.astype(np.int32)
+        else:
+            y = orc.requantize_acc(acc, M, S, out.get("dtype", "u8"), out.get("zero_point", 0),
+                                   out.get("rounding", "upward"), out.get("relu", False), out.get("act_min"),
+                                   out.get("act_max"), axis=1)
+        res.append(np.ascontiguousarray(y.transpose(0, 2, 3, 1)))
+    return np.concatenate(res, 0)
+
+
+def ref_conv_case(case: ConvCase, chunk=16):
+    return ref_conv_lib(case.A, case.W, case.zp_A, case.zp_W, case.bias, case.s_A, case.s_W, case.out_params(),
+                        case.stride, case.pad, case.dil, case.groups, chunk)

@@ -27,3 +27,44 @@ def test_resnet50_full_forward_matches_oracle(fused):
     assert np.array_equal(got.view(np.int32), want.view(np.int32))
     # the forward is not degenerate: logits vary across classes and images
     assert np.unique(got).size > 100 and not np.array_equal(got[0], got[1])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_bench_shards_concatenate_to_one_gpu_output(world):
+    """SURVEY §8e test T3 on the CUDA path: configs[4]'s batch split over `world` ranks with
+    bench.shard_model (each shard planned and launched at its own batch, as rank r would run
+    it) reproduces the 1-GPU output bit for bit.  The ranks are run one after another on this
+    GPU: the sharded path has no collective, so nothing waits on another rank."""
+    import bench
+    from paper_2006_10226_b200.sharding import shard_range
+    G = 40
+    gm = bench.resnet50_model(G)
+    dev = torch.device("cuda")
+    full = bench.GpuResNet50(gm, dev)
+    full.step()
+    torch.cuda.synchronize()
+    want_logits = full.fc_out.cpu().numpy()
+    want_last = full.stack.outs["layer4.2.conv3"].cpu().numpy()
+    got_logits, got_last = [], []
+    for r in range(world):
+        lo, hi = shard_range(G, r, world)
+        net = bench.GpuResNet50(bench.shard_model(gm, lo, hi), dev)
+        net.step()
+        torch.cuda.synchronize()
+        got_logits.append(net.fc_out.cpu().numpy())
+        got_last.append(net.stack.outs["layer4.2.conv3"].cpu().numpy())
+    assert np.array_equal(np.concatenate(got_logits), want_logits)
+    assert np.array_equal(np.concatenate(got_last), want_last)
+    # and the full forward (glue ops) shards the same way
+    fm = bench.resnet50_full_model(G)
+    ffull = bench.GpuResNet50Full(fm, dev)
+    ffull.step()
+    torch.cuda.synchronize()
+    parts = []
+    for r in range(world):
+        lo, hi = shard_range(G, r, world)
+        n = bench.GpuResNet50Full(bench.shard_full_model(fm, lo, hi), dev)
+        n.step()
+        torch.cuda.synchronize()
+        parts.append(n.logits.cpu().numpy())
+    assert np.array_equal(np.concatenate(parts).view(np.int32), ffull.logits.cpu().numpy().view(np.int32))

@@ -87,3 +87,45 @@ def test_bench_reference_arm_runs_on_cpu():
     for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "higher_is_better", "config"):
         assert k in line
     assert line["impl"] == "reference" and line["value"] > 0
+
+
+def test_bench_gpus2_spawns_two_ranks_on_cpu():
+    """`bench.py --gpus 2` without torchrun launches the two ranks itself (127.0.0.1); with the
+    reference arm (no GPU needed) rank 0 prints exactly one JSON line and rank 1 exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=900, cwd=root,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_bench_rejects_world_gpus_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "4",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=root,
+                       env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
+
+
+def test_shard_model_partitions_the_batch():
+    import bench
+    gm = bench.resnet50_model(7)
+    parts = [bench.shard_model(gm, *shard_range(7, r, 3)) for r in range(3)]
+    assert np.array_equal(np.concatenate([p["image"] for p in parts]), gm["image"])
+    assert np.array_equal(np.concatenate([p["fc"]["A"] for p in parts]), gm["fc"]["A"])
+    for k in gm["fresh"]:
+        assert np.array_equal(np.concatenate([p["fresh"][k] for p in parts]), gm["fresh"][k])
+    for p in parts:
+        n = p["image"].shape[0]
+        assert all(sp.N == n for sp in p["specs"])
+        assert p["weights"] is gm["weights"]      # replicated, not re-drawn

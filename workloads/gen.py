@@ -93,9 +93,9 @@ def conv_case(seed: int, N: int, C: int, H: int, W: int, K: int, R: int, S: int,
               act6=False) -> ConvCase:
     g = rng(seed)
     A = rand_q(g, (N, H, W, C), a_dtype)
+    # s8 weights over the full code range, -128 included (a symmetric TFLite-style quantizer would
+    # stop at -127; the kernels must handle the extreme code regardless)
     lo_w, hi_w = _RANGE[w_dtype]
-    if w_dtype == "s8" and zp_W == 0:
-        lo_w = -127                         # symmetric s8 weights (TFLite per-channel convention)
     Wt = rand_q(g, (K, R, S, C // groups), w_dtype, lo_w, hi_w)
     if zp_A is None:
         zp_A = int(g.integers(*_RANGE[a_dtype])) if a_dtype == "u8" else int(g.integers(-64, 64))
@@ -152,9 +152,7 @@ def dense_case(seed: int, M: int, N: int, K: int, a_dtype="u8", w_dtype="s8", zp
                bias=True) -> DenseCase:
     g = rng(seed)
     A = rand_q(g, (M, K), a_dtype)
-    lo_w, hi_w = _RANGE[w_dtype]
-    if w_dtype == "s8" and zp_W == 0:
-        lo_w = -127
+    lo_w, hi_w = _RANGE[w_dtype]   # full code range, -128 included
     Wt = rand_q(g, (N, K), w_dtype, lo_w, hi_w)
     if zp_A is None:
         zp_A = int(g.integers(1, 255)) if a_dtype == "u8" else int(g.integers(-64, 64))
