@@ -205,6 +205,9 @@ struct ConvPlan {
   // 16-B aligned output, else the pixel-major kernel runs on pk_w
   bool trans = false, t_wres = false;
   int t_stages = 0, t_Kt = 0, t_bufs = 1;
+  // channel-major build mode (small-C stems with K_out <= 64): X' built in smem by the idle quads
+  bool t_build = false;
+  int t_ib = 0, t_nr = 0, t_slot = 0, t_raw = 0, t_rstages = 0;
   size_t pk_wt = 0;
   size_t pk_w = 0, pk_off = 0, pk_off64 = 0, pk_dwtc_w = 0, pk_mult = 0, pk_rsh = 0, pk_rowcls = 0, pk_colcls = 0, pk_bias = 0, pk_total = 0;
   // workspace layout
@@ -544,13 +547,50 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       }
     }
   }
+  {
+    // small-C stems with K_out <= 64 (ResNet-50 7x7x3, Inception-v3 / MobileNet-v2 3x3x3): the
+    // channel-major GEMM in build mode -- its quads 2-3 (no output channels) build the X' tiles
+    // and the epilogue keeps per-channel constants in registers.  Only where the pixel-major
+    // builder (a_build, same zp_A fill, same single border class) is the fallback for a
+    // misaligned output.  QNN_NO_TBUILD=1 keeps the pixel-major kernel (A/B measurements).
+    static const bool no_tbuild = std::getenv("QNN_NO_TBUILD") != nullptr;
+    const long long rowlen = (long long)d->W * d->C;
+    if (!no_tbuild && pl.a_build && pl.a_zpfill && d->K <= 64 && d->K % 32 == 0 && d->dil_h == 1 &&
+        d->kernel_dtype == QNN_S8 && (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && pl.out_cs % 16 == 0 &&
+        d->R <= 16) {
+      int ib = 0;
+      for (int c : {256, 128, 64, 32, 16})
+        if (rowlen % c == 0 && rowlen / c <= 256) {
+          ib = c;
+          break;
+        }
+      const int nr = (kGemmTBN - 1) / pl.Q + 2;
+      const int slot = (int)((d->R * rowlen + 127) / 128 * 128);
+      const int raw = (nr * slot + 1023) / 1024 * 1024;
+      // two X' stages; the raw-row ring as deep as the rest of shared memory allows (<= 6)
+      int rst = 0;
+      for (int r = 6; r >= 2 && !rst; --r)
+        if (gemm_t_smem_bytes(32, d->R, 2, true, 1, raw, r, d->K) <= 226 * 1024) rst = r;
+      if (ib && rst) {
+        pl.trans = pl.t_build = pl.t_wres = true;
+        pl.t_stages = 2;
+        pl.t_rstages = rst;
+        pl.t_bufs = 1;
+        pl.t_Kt = 128;
+        pl.t_ib = ib;
+        pl.t_nr = nr;
+        pl.t_slot = slot;
+        pl.t_raw = raw;
+      }
+    }
+  }
   const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
   off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
   if (pl.trans) {
     pl.pk_wt = off;
-    off = align256(off + (size_t)pl.t_Kt * pl.Cw);
+    off = align256(off + (size_t)pl.t_Kt * taps * pl.Cw);
   }
   pl.pk_off = off;
   off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
@@ -643,7 +683,8 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
     else
       e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
     if (e == cudaSuccess && pl.trans)
-      e = launch_pack_weights(kernel, pk + pl.pk_wt, d->K, 1, d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1);
+      e = pl.fold ? launch_pack_weights(kernel, pk + pl.pk_wt, d->K, d->R, d->S * d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1)
+                  : launch_pack_weights(kernel, pk + pl.pk_wt, d->K, 1, d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
                             pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off),
@@ -833,10 +874,29 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
       alignas(64) CUtensorMap tmX, tmW, tmC, tmR;
       std::memset(&tmR, 0, sizeof(tmR));
       const int a_chan = d->C;
-      bool okt = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmTBN) &&
-                 encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)pl.Cw, (uint64_t)pl.t_Kt, (uint64_t)pl.Cw, pl.BK, 128) &&
-                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, 128, kGemmTBN / 4) &&
-                 (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, 128,
+      bool okx;
+      const int taps = d->R * pl.gS;
+      // staging / store rows: one 128-channel block, or K_out (64 / 32) bytes in build mode
+      const uint32_t out_rb = pl.t_build ? (uint32_t)d->K : 128u;
+      if (pl.t_build) {
+        // raw input rows as (ib bytes, W*C/ib, H, N): one box = the R filter rows of one output row
+        const uint64_t rowlen = (uint64_t)d->W * d->C;
+        const cuuint64_t dims[4] = {(cuuint64_t)pl.t_ib, rowlen / pl.t_ib, (cuuint64_t)d->H, (cuuint64_t)d->N};
+        const cuuint64_t strides[3] = {(cuuint64_t)pl.t_ib, rowlen, rowlen * d->H};
+        const cuuint32_t box[4] = {(cuuint32_t)pl.t_ib, (cuuint32_t)(rowlen / pl.t_ib), (cuuint32_t)d->R, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        okx = p_encode_tiled(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(input), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        small_tensor_fixup(&tmX, rowlen * d->H * d->N);
+      } else {
+        okx = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmTBN);
+      }
+      bool okt = okx &&
+                 encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)taps * pl.Cw, (uint64_t)pl.t_Kt, (uint64_t)taps * pl.Cw, pl.BK,
+                           128) &&
+                 encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, out_rb, kGemmTBN / 4) &&
+                 (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, out_rb,
                                     kGemmTBN / 4));
       if (okt) {
         GemmTParams tp{};
@@ -845,6 +905,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         tp.num_kb = num_kb;
         tp.w_res = w_res;
         tp.stage_bufs = pl.t_bufs;
+        tp.out_rb = (int)out_rb;
         tp.num_ch_tiles = (d->K + 127) / 128;
         tp.Kout = d->K;
         if (res) {
@@ -855,6 +916,21 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
           tp.res_s8 = res->dtype == QNN_S8;
         }
         tp.num_px_tiles = (int)((pl.M + kGemmTBN - 1) / kGemmTBN);
+        if (pl.t_build) {
+          tp.build = 1;
+          tp.num_kb = d->R;   // one 32-byte k-block (S*C bytes) per filter row
+          tp.b_W = d->W; tp.b_C = d->C; tp.b_S = d->S; tp.b_sw = d->stride_w; tp.b_pl = d->pad_l;
+          tp.b_rowlen = d->W * d->C;
+          tp.b_nr = pl.t_nr;
+          tp.b_H = d->H;
+          tp.b_slot_bytes = pl.t_slot;
+          tp.b_raw_bytes = pl.t_raw;
+          tp.rstages = pl.t_rstages;
+          tp.b_zp4 = 0x01010101u * (uint32_t)(d->input_zero_point & 0xFF);
+          tp.P = pl.P; tp.Q = pl.Q; tp.sh = d->stride_h; tp.pt = d->pad_t;
+          tp.fdQ = make_fastdiv((uint32_t)pl.Q);
+          tp.fdP = make_fastdiv((uint32_t)pl.P);
+        }
         tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights, B = activations
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
         tp.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
@@ -866,6 +942,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         {
           static const char* dbg_env = std::getenv("QNN_GEMM_DEBUG");
           tp.dbg = dbg_env ? std::atoi(dbg_env) : 0;
+          static const char* tr_env = std::getenv("QNN_GEMM_TRACE");
+          tp.trace = tr_env ? reinterpret_cast<unsigned long long*>(std::strtoull(tr_env, nullptr, 0)) : nullptr;
         }
 #endif
         const int sms = sm_count();

@@ -46,21 +46,34 @@ constexpr bool kTInstrument = true;    // QNN_GEMM_DEBUG knobs compiled in (prof
 constexpr bool kTInstrument = false;
 #endif
 
+// CTA 0 event timestamps (instrumented builds): slot ranges per role, 64 tiles each
+//   0: producer issue, 64: builder start (after its waits), 128: builder done, 192: MMA start,
+//   256: MMA commit, 320: epilogue tfull wake (warp 0), 384: epilogue store issued (warp 0)
+__device__ __forceinline__ void t_trace(const unsigned long long* tr, int slot, int it) {
+  if (kTInstrument && tr && blockIdx.x == 0 && it < 64) const_cast<unsigned long long*>(tr)[slot + it] = clock64();
+}
+
 constexpr int kTEpiWarps = 16;
 constexpr int kTThreads = 32 * kTEpiWarps + 64;
 constexpr int kTBM = 128;   // output channels per tile (MMA M)
 constexpr int kTBN = kGemmTBN;          // pixels per tile (MMA N), internal.h
 constexpr int kTNacc = 512 / kTBN;      // TMEM accumulator buffers (512 columns)
+// epilogue: warp (quad, grp) reads its quad's 32 TMEM lanes and pixel columns [grp * kTCols,
+// +kTCols) of every tile (a variant with two warp sets taking alternate tiles, 128 columns
+// per warp, measured 10-20% slower)
 constexpr int kTCols = kTBN / 4;        // pixel columns per epilogue warp (4 column groups)
-constexpr int kTHalves = kTCols / 32;   // 32-column steps per warp and tile
 // output staging, per column group (the 4 warps of one group of pixel columns share it):
 // [kTCols pixels][128 channels] in the TMA 128-B swizzle (16-B chunk c of row r at chunk
 // c ^ (r % 8)), one TMA store of 128-B rows per group and tile; 1 or 2 buffers (host choice)
-constexpr int kTGroupOut = kTCols * 128;
 #ifdef QNN_T_SPIN
 #define QNN_T_WAIT mbar_wait_spin
 #else
 #define QNN_T_WAIT mbar_wait
+#endif
+#ifdef QNN_T_EPI_SPIN
+#define QNN_TEPI_WAIT mbar_wait_spin
+#else
+#define QNN_TEPI_WAIT QNN_EPI_WAIT
 #endif
 
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
@@ -91,6 +104,15 @@ __device__ __forceinline__ void tmem_wait16x2(uint32_t (&a)[16], uint32_t (&b)[1
                  "+r"(b[14]), "+r"(b[15])
                :
                : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d_t(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2,
+                                              int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
 }
 
 // the residual byte requantized to the output scale with zero point 0 (reading R19: added
@@ -124,14 +146,14 @@ __device__ __forceinline__ int32_t tq1(const TChan& q, int i, uint32_t acc, int3
 // pack 4 channels per word, store into the staging tile [pixel][32 channels]
 template <int MODE, bool FAST, bool CLAMP, bool S8OUT, bool RES>
 __device__ __forceinline__ void t_epilogue(const GemmTParams& p, const TChan& q, const uint32_t (&va)[16],
-                                           const uint32_t (&vb)[16], uint32_t st0, uint32_t st1) {
+                                           const uint32_t (&vb)[16], uint32_t st0, uint32_t st1, uint32_t rb) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       // pixel column 8k + 2u + e of this 32-column step; channels 4j + i from lanes j, j+8 (va)
       // and j+16, j+24 (vb); the swizzled word address depends on e and the thread only
-      const uint32_t a = (e ? st1 : st0) + (uint32_t)(8 * k * 128);
+      const uint32_t a = (e ? st1 : st0) + (uint32_t)(8 * k) * rb;
       int32_t y[4];
       y[0] = tq1<MODE, FAST>(q, 0, va[4 * k + e], p.zp_out);
       y[1] = tq1<MODE, FAST>(q, 1, va[4 * k + 2 + e], p.zp_out);
@@ -156,16 +178,22 @@ __device__ __forceinline__ void t_epilogue(const GemmTParams& p, const TChan& q,
 constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers are static)
 
 // w_res: the CTA's weight block stays resident (num_kb blocks); otherwise each pipeline stage
-// carries its weight k-block next to the activation k-block
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs) {
-  const size_t stage = (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK);
-  return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK : 0) +
-         (size_t)4 * kTGroupOut * stage_bufs + 256;
+// carries its weight k-block next to the activation k-block.  build_raw_bytes >= 0: build mode,
+// a stage holds all num_kb X' k-blocks of a tile plus its raw input rows (weights resident)
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes,
+                         int rstages, int out_rb) {
+  const size_t stage = build_raw_bytes >= 0 ? (size_t)num_kb * kTBN * BK
+                                            : (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK);
+  const size_t raw = build_raw_bytes >= 0 ? (size_t)rstages * build_raw_bytes : 0;
+  return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK : 0) + raw +
+         (size_t)4 * kTCols * out_rb * stage_bufs + 256;
 }
 
-int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs) {
+int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes, int rstages, int out_rb) {
   int s = 8;
-  while (s > 2 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs) > (size_t)kTSmemMax) --s;
+  while (s > 1 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs, build_raw_bytes, rstages, out_rb) >
+                      (size_t)kTSmemMax)
+    --s;
   return s;
 }
 
@@ -179,10 +207,19 @@ __global__ void __launch_bounds__(kTThreads, 1)
   const int BK = p.BK, stages = p.stages, num_kb = p.num_kb;
   const uint32_t x_bytes = (uint32_t)kTBN * BK, w_bytes = (uint32_t)kTBM * BK;
   const bool w_res = p.w_res;
-  uint8_t* sX = smem;                                  // stages x [256 pixels][BK]
-  uint8_t* sW = sX + (size_t)stages * x_bytes;         // num_kb (resident) or stages x [128 channels][BK]
-  uint8_t* sOut = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // 16 x [64 pixels][32 channels]
-  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[4];
+  const bool build = p.build;
+  // X: stages x [256 pixels][BK] (build mode: stages x num_kb x [256 pixels][32], built in smem)
+  const size_t x_stage = build ? (size_t)num_kb * x_bytes : (size_t)x_bytes;
+  uint8_t* sX = smem;
+  uint8_t* sW = sX + (size_t)stages * x_stage;         // num_kb (resident) or stages x [128 channels][BK]
+  uint8_t* sRaw = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // build: stages x raw input rows
+  uint8_t* sOut = sRaw + (build ? (size_t)p.rstages * p.b_raw_bytes : 0);   // 4 groups x [kTCols px][out_rb]
+  const uint32_t out_rb = (uint32_t)p.out_rb;   // staging row bytes: 128, or 64 / 32 when K_out is 64 / 32
+  // epilogue warps: the quads holding live channels (all 4, or K_out / 32 in build mode, whose
+  // quads 2 and 3 build the X' tiles)
+  const int ep_quads = build ? (p.Kout + 31) / 32 : 4;
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[4], rawfull[8],
+      rawempty[8];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = kTEpiWarps, kMmaWarp = kTEpiWarps + 1;
@@ -195,12 +232,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
     tma_prefetch_desc(&tmC);
     if (RES) tma_prefetch_desc(&tmR);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], build ? 8 : 1);   // build mode: one arrive per builder warp
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < p.rstages; ++s) {
+      mbar_init(&rawfull[s], 1);
+      mbar_init(&rawempty[s], 8);   // build mode: every builder warp has read the raw rows
     }
     for (int a = 0; a < kTNacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kTEpiWarps);
+      mbar_init(&tempty[a], 4 * ep_quads);   // 4 column groups x live quads
     }
     mbar_init(&wfull, 1);
     for (int g = 0; g < 4; ++g) mbar_init(&rbar[g], 1);
@@ -220,9 +261,35 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     int stage = 0;
     uint32_t phase = 0;
-    for (int pt = px_first; pt < npt; pt += px_step) {
+    if (build) {
+      // per tile: the R input rows of every output row the tile touches, one 4-D box each
+      // (zero outside the image; the builders write zp_A there)
+      // (raw rows have their own ring of rstages, deeper than the X' ring: the loads run ahead
+      // of the builders by rstages tiles)
+      const uint32_t bytes = (uint32_t)p.b_nr * num_kb * p.b_rowlen;
+      for (int pt = px_first; pt < npt; pt += px_step) {
+        const int r_first = (int)fdiv((uint32_t)(pt * kTBN), p.fdQ);
+        QNN_T_WAIT(&rawempty[stage], phase ^ 1);
+        if (leader) {
+          t_trace(p.trace, 0, (pt - px_first) / px_step);
+          mbar_arrive_expect_tx(&rawfull[stage], bytes);
+          uint8_t* dst = sRaw + (size_t)stage * p.b_raw_bytes;
+          for (int k = 0; k < p.b_nr; ++k) {
+            const int ri = r_first + k, n = (int)fdiv((uint32_t)ri, p.fdP), pp = ri - n * p.P;
+            tma_load_4d_t(dst + (size_t)k * p.b_slot_bytes, &tmX, &rawfull[stage], 0, 0, pp * p.sh - p.pt, n);
+          }
+        }
+        __syncwarp();
+        if (++stage == p.rstages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    for (int pt = build ? npt : px_first; pt < npt; pt += px_step) {
       for (int kb = 0; kb < num_kb; ++kb) {
         QNN_T_WAIT(&empty[stage], phase ^ 1);
+        if (leader && kb == 0) t_trace(p.trace, 0, (pt - px_first) / px_step);
         if (leader) {
           mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes));
           tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
@@ -247,13 +314,35 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const int acc = it % kTNacc;
       QNN_T_WAIT(&tempty[acc], ((it / kTNacc) & 1) ^ 1);
       tc_fence_after();
+      if (!build && leader) t_trace(p.trace, 64, it);   // (non-build: slot 64 = accumulator free)
       const uint32_t d = tmem_base + (uint32_t)acc * kTBN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      if (build) {
+        // one stage = the whole tile: num_kb X' k-blocks (32 bytes = one K step each)
         QNN_T_WAIT(&full[stage], phase);
         tc_fence_after();
         if (leader) {
-          const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage) * w16, xd = xdesc0 + (uint64_t)stage * x16;
-          for (int k = 0; k < ksteps; ++k) umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+          t_trace(p.trace, 192, it);
+          const uint64_t xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
+          for (int kb = 0; kb < num_kb; ++kb) umma_i8(d, wdesc0 + (uint64_t)kb * w16, xd + (uint64_t)kb * x16, idesc, kb != 0);
+          umma_commit(&empty[stage]);
+          umma_commit(&tfull[acc]);
+          t_trace(p.trace, 256, it);
+        }
+        __syncwarp();
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
+      for (int kb = 0; kb < num_kb; ++kb) {
+        QNN_T_WAIT(&full[stage], phase);
+        tc_fence_after();
+        if (leader && kb == 0) t_trace(p.trace, 192, it);
+        if (leader) {
+          const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage) * w16, xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
+          if (!(kTInstrument && (p.dbg & 8)))   // (instrumented builds: 8 skips the MMAs)
+            for (int k = 0; k < ksteps; ++k) umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -262,10 +351,95 @@ __global__ void __launch_bounds__(kTThreads, 1)
           phase ^= 1;
         }
       }
-      if (leader) umma_commit(&tfull[acc]);
+      if (leader) {
+        umma_commit(&tfull[acc]);
+        t_trace(p.trace, 256, it);
+      }
       __syncwarp();
     }
-  } else if (warp < kTEpiWarps) {
+  } else if (build && (warp & 3) >= 2) {
+    // ---------------------------------------------------------------- X' builders (build mode)
+    // thread bt (8 warps = 256 threads) owns pixel bt of every tile: for each filter row r the
+    // S*C bytes of raw row (p, r) from column q*sw - pl on (zp_A outside the image), in the
+    // 32-B swizzle of the UMMA K-major B operand.  Bytes past S*C are left as they come: the
+    // packed weights are zero there.
+    const int bt = ((warp >> 2) * 2 + ((warp & 3) - 2)) * 32 + lane;
+    const int SC = p.b_S * p.b_C, rowlen = p.b_rowlen;
+    const uint32_t swz = ((uint32_t)bt >> 2) & 1u;
+    const uint32_t fill = p.b_zp4;
+    int stage = 0, rstage = 0;
+    uint32_t phase = 0, rphase = 0;
+    for (int pt = px_first; pt < npt; pt += px_step) {
+      const int m0 = pt * kTBN;
+      const int r_first = (int)fdiv((uint32_t)m0, p.fdQ);
+      const int row = m0 + bt;
+      const int ri = (int)fdiv((uint32_t)row, p.fdQ), qq = row - ri * p.Q;
+      const int o = (qq * p.b_sw - p.b_pl) * p.b_C;   // window start in the row (may be < 0)
+      const int ab = o & ~3;
+      const uint32_t sh8 = (uint32_t)(o - ab) * 8u;
+      const bool border = o < 0 || o + SC > rowlen;
+      uint32_t mk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mk[k] = 0xFFFFFFFFu;
+      if (border) {
+        const int jlo = max(0, -o), jhi = min(SC, rowlen - o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int l = min(max(jlo - 4 * k, 0), 4), h = min(max(jhi - 4 * k, 0), 4);
+          const uint32_t mh = h == 4 ? 0xFFFFFFFFu : ((1u << (8 * h)) - 1u);
+          const uint32_t ml = l == 4 ? 0xFFFFFFFFu : ((1u << (8 * l)) - 1u);
+          mk[k] = h > l ? (mh & ~ml) : 0u;
+        }
+      }
+      const int h0 = (ri - (int)fdiv((uint32_t)ri, p.fdP) * p.P) * p.sh - p.pt;   // input row of filter row 0
+      QNN_EPI_WAIT(&empty[stage], phase ^ 1);
+      QNN_EPI_WAIT(&rawfull[rstage], rphase);
+      if (bt == 0) t_trace(p.trace, 64, (pt - px_first) / px_step);
+      const uint8_t* rp0 = sRaw + (size_t)rstage * p.b_raw_bytes + (size_t)(ri - r_first) * p.b_slot_bytes + ab;
+      uint8_t* dA = sX + (size_t)stage * x_stage + (size_t)bt * 32;
+      // (measured: software-pipelining the row loads across rows does not help -- the stem is
+      // bound by shared-memory bandwidth: raw-row reads, X' writes and the MMA's operand reads)
+#pragma unroll 4
+      for (int r = 0; r < num_kb; ++r) {
+        // 9 aligned words around the window (addresses outside the row only feed masked bytes
+        // and stay inside this CTA's shared memory)
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(rp0 + (size_t)r * rowlen);
+        uint32_t uw[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) uw[k] = wp[k];
+        uint32_t wv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wv[k] = __funnelshift_r(uw[k], uw[k + 1], sh8);
+        if (border) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wv[k] = (wv[k] & mk[k]) | (fill & ~mk[k]);
+        }
+        const int hh = h0 + r;
+        if (hh < 0 || hh >= p.b_H) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wv[k] = fill;
+        }
+        uint8_t* rowdst = dA + (size_t)r * x_bytes;
+        *reinterpret_cast<uint4*>(rowdst + (swz << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4*>(rowdst + ((swz ^ 1u) << 4)) = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (bt == 0) t_trace(p.trace, 128, (pt - px_first) / px_step);
+        mbar_arrive(&full[stage]);
+        mbar_arrive(&rawempty[rstage]);
+      }
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (++rstage == p.rstages) {
+        rstage = 0;
+        rphase ^= 1;
+      }
+    }
+  } else if (warp < kTEpiWarps && (warp & 3) < ep_quads) {
     // ---------------------------------------------------------------- epilogue
     const int quad = warp & 3, grp = warp >> 2;
     const int j = lane >> 2, u = lane & 3;
@@ -294,62 +468,74 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     const int dbg = kTInstrument ? p.dbg : 0;
     const bool all_fast = __all_sync(0xffffffffu, fast);
-    // column group grp shares a [kTCols][128] staging tile (1 or 2 buffers) with the other 3
-    // quads; its quad-0 lane 0 issues the group's TMA store (and residual load)
+    // column group grp shares a [kTCols][out_rb] staging tile (1 or 2 buffers) with the other
+    // live quads; its quad-0 lane 0 issues the group's TMA store (and residual load)
     const bool gleader = quad == 0 && lane == 0;
     const int nbufs = p.stage_bufs;
-    uint8_t* const gstage = sOut + (size_t)grp * kTGroupOut * nbufs;
-    // this thread's words (pixel rows 2u + e, e = 0/1; channel word 8 quad + j) in the 128-B swizzle
+    const uint32_t gbytes = (uint32_t)kTCols * out_rb;   // one group's staging buffer
+    uint8_t* const gstage = sOut + (size_t)grp * gbytes * nbufs;
+    // this thread's words (pixel rows 2u + e, e = 0/1; channel word 8 quad + j) in the TMA
+    // swizzle of out_rb-byte rows: 16-B chunk c of row r sits at chunk c ^ (r / (128 / out_rb))
+    // mod (out_rb / 16) -- for the rows 2u + e (+ 8k + 32h) of one store that is 2u + e at
+    // 128 B, u at 64 B and u / 2 at 32 B
     const uint32_t ch16 = (uint32_t)(2 * quad + (j >> 2));
-    const uint32_t st_off0 = (uint32_t)(2 * u) * 128 + ((ch16 ^ (uint32_t)(2 * u)) << 4) + (uint32_t)((j & 3) << 2);
-    const uint32_t st_off1 = (uint32_t)(2 * u + 1) * 128 + ((ch16 ^ (uint32_t)(2 * u + 1)) << 4) +
-                             (uint32_t)((j & 3) << 2);
+    const uint32_t sw0 = out_rb == 128 ? (uint32_t)(2 * u) : (out_rb == 64 ? (uint32_t)u : (uint32_t)(u >> 1));
+    const uint32_t sw1 = out_rb == 128 ? (uint32_t)(2 * u + 1) : sw0;
+    const uint32_t st_off0 = (uint32_t)(2 * u) * out_rb + ((ch16 ^ sw0) << 4) + (uint32_t)((j & 3) << 2);
+    const uint32_t st_off1 = (uint32_t)(2 * u + 1) * out_rb + ((ch16 ^ sw1) << 4) + (uint32_t)((j & 3) << 2);
     int it = 0;
     for (int pt = px_first; pt < npt; pt += px_step, ++it) {
       const int acc = it % kTNacc;
-      uint8_t* const stage_out = gstage + (nbufs == 2 ? (it & 1) * kTGroupOut : 0);
+      uint8_t* const stage_out = gstage + (nbufs == 2 ? (it & 1) * gbytes : 0);
       const uint32_t sbase = smem_u32(stage_out);
+      const int col0 = pt * kTBN + grp * kTCols;
       if (gleader) {
         bulk_wait_read_dyn(nbufs - 1);   // the store that last used this buffer has read it
         if (RES) {
-          // the residual tile (this group's pixels x 128 channels, same swizzle) lands in the
+          // the residual tile (this group's pixels x out_rb channels, same swizzle) lands in the
           // staging buffer; each thread reads its four channels' word per pixel and overwrites it
-          mbar_arrive_expect_tx(&rbar[grp], kTGroupOut);
-          tma_load_2d(stage_out, &tmR, &rbar[grp], ch * kTBM, pt * kTBN + grp * kTCols);
+          mbar_arrive_expect_tx(&rbar[grp], gbytes);
+          tma_load_2d(stage_out, &tmR, &rbar[grp], ch * kTBM, col0);
         }
       }
-      named_bar_sync(1 + grp, 128);      // the buffer is free for every warp of the group
-      QNN_EPI_WAIT(&tfull[acc], (it / kTNacc) & 1);
+      named_bar_sync(1 + grp, 32 * ep_quads);   // the buffer is free for every warp of the group
+      QNN_TEPI_WAIT(&tfull[acc], (it / kTNacc) & 1);
       tc_fence_after();
+      if (warp == 0 && lane == 0) t_trace(p.trace, 320, it);
       const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * kTCols);
       if (RES) mbar_wait(&rbar[grp], (uint32_t)(it & 1));
-      // steps of 32 pixel columns (register budget: 96 per thread at 18 warps)
-#pragma unroll 1
-      for (int h = 0; h < kTHalves; ++h) {
-        uint32_t va[16], vb[16];
-        tmem_ld_16x256b_x4(tb + 32 * h, va);                  // lanes j, j + 8
-        tmem_ld_16x256b_x4(tb + 32 * h + (16u << 16), vb);    // lanes j + 16, j + 24
-        tmem_wait16x2(va, vb);
-        if (h == kTHalves - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        const uint32_t rowb = sbase + (uint32_t)(h * 32 * 128);
-        // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
-        if ((dbg & 1) || !quad_live) {
-        } else if (all_fast) {
-          t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va, vb, rowb + st_off0, rowb + st_off1);
-        } else {
-          t_epilogue<MODE, false, CLAMP, S8OUT, RES>(p, q, va, vb, rowb + st_off0, rowb + st_off1);
-        }
+      // all four TMEM loads in flight at once, one wait, and the accumulator handed back to the
+      // MMA warp before any math
+      uint32_t va0[16], vb0[16], va1[16], vb1[16];
+      if (!(dbg & 16)) {   // (instrumented builds: 16 skips the TMEM loads)
+        tmem_ld_16x256b_x4(tb, va0);                         // lanes j, j + 8, columns 0..31
+        tmem_ld_16x256b_x4(tb + (16u << 16), vb0);           // lanes j + 16, j + 24
+        tmem_ld_16x256b_x4(tb + 32, va1);                    // columns 32..63
+        tmem_ld_16x256b_x4(tb + 32 + (16u << 16), vb1);
+        tmem_wait16x2(va0, vb0);
+        tmem_wait16x2(va1, vb1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
+      if ((dbg & 1) || !quad_live) {
+      } else if (all_fast) {
+        t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
+        t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
+                                                  sbase + 32 * out_rb + st_off1, out_rb);
+      } else {
+        t_epilogue<MODE, false, CLAMP, S8OUT, RES>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
+        t_epilogue<MODE, false, CLAMP, S8OUT, RES>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
+                                                   sbase + 32 * out_rb + st_off1, out_rb);
       }
       fence_proxy_async_smem();
-      named_bar_sync(1 + grp, 128);      // every warp of the group has written its channels
+      named_bar_sync(1 + grp, 32 * ep_quads);   // every warp of the group has written its channels
       if (gleader && !(dbg & 2)) {
-        tma_store_2d(&tmC, stage_out, ch * kTBM, pt * kTBN + grp * kTCols);
+        tma_store_2d(&tmC, stage_out, ch * kTBM, col0);
         bulk_commit();
       }
+      if (warp == 0 && lane == 0) t_trace(p.trace, 384, it);
     }
     if (gleader) bulk_wait_all();
     __syncwarp();
@@ -366,7 +552,8 @@ cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream) {
   const bool res = p.has_res;
-  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res, p.stage_bufs);
+  const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res, p.stage_bufs,
+                                       p.build ? p.b_raw_bytes : -1, p.rstages, p.out_rb);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);

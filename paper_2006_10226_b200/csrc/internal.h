@@ -80,10 +80,23 @@ struct GemmTParams {
   const int64_t* off64;  // [Kpad] (single border class)
   int32_t zp_out, lo, hi;
   int stage_bufs;         // output staging buffers per column group (1 or 2)
+  int out_rb;             // staging / TMA-store row bytes: 128 (min(K_out, 128) in build mode)
+  // build mode (small-C stems, K_out <= 64): the B operand X'[pixel][s*C + c] (one 32-byte
+  // k-block per filter row, width fold of P:259's zero-point-padded input) is built in shared
+  // memory by the warps of the unused quads 2 and 3 from TMA-staged raw input rows
+  int build;
+  int b_W, b_C, b_S, b_sw, b_pl, b_rowlen, b_nr, b_H, b_slot_bytes, b_raw_bytes;
+  int rstages;            // raw-row ring depth (build mode)
+  uint32_t b_zp4;         // zp_A in all four bytes (written outside the image: one border class)
+  int P, Q, sh, pt;
+  FastDiv fdQ, fdP;
   int dbg;   // QNN_GEMM_DEBUG (instrumented builds only): 1 skips the epilogue math, 2 the TMA stores
+  unsigned long long* trace;   // QNN_GEMM_TRACE (instrumented builds only): CTA 0 clock64 events
 };
-size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs);
-int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs);
+size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes = -1,
+                         int rstages = 0, int out_rb = 128);
+int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes = -1, int rstages = 0,
+                      int out_rb = 128);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream);
