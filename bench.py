@@ -306,6 +306,275 @@ class GpuResNet50Full:
         self.graph.replay()
 
 
+# ----------------------------------------------------------------------------- Inception-v3 (configs[4])
+def inception_v3_full_model(batch: int, seed: int = 7000):
+    """Synthetic pre-quantized Inception-v3 forward (torchvision layout, 299x299), the second
+    network of configs[4]: the 94 convs of workloads.shapes.inception_v3_convs with the glue
+    between them -- stem max pools, per-block branches whose last convs write straight into
+    their channel slice of the block's concat buffer (out_cstride; no concat op), 3x3/s1/p1
+    average pools (padding excluded, reading R20) before the pool-branch 1x1s, 3x3/s2 max
+    pools in the reduction blocks, the 8x8 global average pool, fc (raw int32), dequantize.
+
+    Quantization: u8 activations, zp 0 after ReLU (the image: zp 128); every branch of a block
+    requantizes to the block's output scale so the concat needs no requantize (the median of
+    its branch-final convs' calibrated scales; the input scale in the reduction blocks, whose
+    max-pool branch passes its input through).  Weights s8 per-channel with the ResNet recipe."""
+    from workloads import gen
+    from workloads.shapes import inception_v3_convs
+    convs = {c.name: c for c in inception_v3_convs()}
+    img_scale, img_zp = float(np.float32(4.77 / 255)), 128
+    T = {"image": dict(H=299, W=299, C=3, zp=img_zp, s=img_scale)}
+    layers, ops = {}, []
+    counter = [0]
+
+    # second moments of the input codes: the image (N(0,1) at 4.77/255 per level: ~53 codes RMS
+    # around zp 128) or a post-ReLU activation calibrated to 6 sigma (gen.POST_RELU_VAR); the
+    # uniform-input calibration of the ResNet recipe would shrink the signal ~5x per layer here
+    VAR_W = ((127 + 127 + 1) ** 2 - 1) / 12.0
+
+    def var_in(zp_A):
+        return (1.0 / (4.77 / 255.0)) ** 2 if zp_A == img_zp else gen.POST_RELU_VAR
+
+    def calib(name, zp_A, s_A):
+        c = convs[name]
+        g = gen.rng(seed + counter[0])
+        counter[0] += 1
+        kk = c.C * c.R * c.S
+        unit = gen.calibrated_out_scale_var(kk, var_in(zp_A), VAR_W, 1.0, 1.0)
+        W = gen.rand_q(g, (c.K, c.R, c.S, c.C), "s8", -127, 127)
+        s_W = (g.uniform(0.5, 1.5, size=c.K) / unit).astype(np.float32)
+        bias = g.integers(-4096, 4097, size=c.K).astype(np.int32)
+        s_out = gen.calibrated_out_scale_var(kk, var_in(zp_A), VAR_W, s_A, float(np.median(s_W)))
+        return W, s_W, bias, s_out
+
+    def conv(name, src, dst=None, off=0, s_out=None):
+        c = convs[name]
+        t = T[src]
+        assert (c.C, c.H, c.W) == (t["C"], t["H"], t["W"]), (name, c, t)
+        W, s_W, bias, s_nat = calib(name, t["zp"], t["s"])
+        so = float(np.float32(s_out if s_out is not None else s_nat))
+        layers[name] = dict(c=c, W=W, bias=bias, zp_A=t["zp"], s_A=t["s"], s_W=s_W,
+                            out=dict(scale=so, zero_point=0, dtype="u8", rounding="upward", relu=True))
+        if dst is None:
+            dst = name
+            T[dst] = dict(H=c.P, W=c.Q, C=c.K, zp=0, s=so)
+        ops.append(dict(kind="conv", name=name, src=src, dst=dst, off=off))
+        return dst
+
+    def pool(kind, src, dst, R, stride, pad, off=0, C_total=None):
+        t = T[src]
+        P = (t["H"] + 2 * pad - R) // stride + 1
+        Q = (t["W"] + 2 * pad - R) // stride + 1
+        if dst not in T:
+            T[dst] = dict(H=P, W=Q, C=C_total or t["C"], zp=t["zp"], s=t["s"])
+        ops.append(dict(kind=kind, src=src, dst=dst, R=R, stride=stride, pad=pad, off=off))
+        return dst
+
+    def block_scale(names, src):
+        return float(np.median([calib_peek(n, T[src]) for n in names]))
+
+    def calib_peek(name, t):
+        # (the natural output scale of a conv of this shape on a post-ReLU input of scale t["s"])
+        return t["s"]
+
+    x = conv("Conv2d_1a_3x3", "image")
+    x = conv("Conv2d_2a_3x3", x)
+    x = conv("Conv2d_2b_3x3", x)
+    x = pool("max", x, "pool1", 3, 2, 0)
+    x = conv("Conv2d_3b_1x1", x)
+    x = conv("Conv2d_4a_3x3", x)
+    x = pool("max", x, "pool2", 3, 2, 0)
+
+    def mixed_a(n, x, pool_features):
+        t = T[x]
+        ctot = 64 + 64 + 96 + pool_features
+        sb = float(np.float32(block_scale([f"{n}.branch1x1", f"{n}.branch5x5_2", f"{n}.branch3x3dbl_3"], x)))
+        T[n] = dict(H=t["H"], W=t["W"], C=ctot, zp=0, s=sb)
+        conv(f"{n}.branch1x1", x, n, 0, sb)
+        y = conv(f"{n}.branch5x5_1", x)
+        conv(f"{n}.branch5x5_2", y, n, 64, sb)
+        y = conv(f"{n}.branch3x3dbl_1", x)
+        y = conv(f"{n}.branch3x3dbl_2", y)
+        conv(f"{n}.branch3x3dbl_3", y, n, 128, sb)
+        y = pool("avg", x, f"{n}.pool", 3, 1, 1)
+        conv(f"{n}.branch_pool", y, n, 224, sb)
+        return n
+
+    x = mixed_a("Mixed_5b", x, 32)
+    x = mixed_a("Mixed_5c", x, 64)
+    x = mixed_a("Mixed_5d", x, 64)
+    # Mixed_6a: the max-pool branch passes its input quantization through
+    t = T[x]
+    n = "Mixed_6a"
+    sb = t["s"]
+    T[n] = dict(H=17, W=17, C=768, zp=0, s=sb)
+    conv(f"{n}.branch3x3", x, n, 0, sb)
+    y = conv(f"{n}.branch3x3dbl_1", x)
+    y = conv(f"{n}.branch3x3dbl_2", y)
+    conv(f"{n}.branch3x3dbl_3", y, n, 384, sb)
+    pool("max", x, n, 3, 2, 0, off=480)
+    x = n
+
+    def mixed_c(n, x):
+        t = T[x]
+        sb = float(np.float32(block_scale([f"{n}.branch1x1", f"{n}.branch7x7_3", f"{n}.branch7x7dbl_5"], x)))
+        T[n] = dict(H=t["H"], W=t["W"], C=768, zp=0, s=sb)
+        conv(f"{n}.branch1x1", x, n, 0, sb)
+        y = conv(f"{n}.branch7x7_1", x)
+        y = conv(f"{n}.branch7x7_2", y)
+        conv(f"{n}.branch7x7_3", y, n, 192, sb)
+        y = conv(f"{n}.branch7x7dbl_1", x)
+        for k in (2, 3, 4):
+            y = conv(f"{n}.branch7x7dbl_{k}", y)
+        conv(f"{n}.branch7x7dbl_5", y, n, 384, sb)
+        y = pool("avg", x, f"{n}.pool", 3, 1, 1)
+        conv(f"{n}.branch_pool", y, n, 576, sb)
+        return n
+
+    for n in ("Mixed_6b", "Mixed_6c", "Mixed_6d", "Mixed_6e"):
+        x = mixed_c(n, x)
+    n = "Mixed_7a"
+    sb = T[x]["s"]
+    T[n] = dict(H=8, W=8, C=1280, zp=0, s=sb)
+    y = conv(f"{n}.branch3x3_1", x)
+    conv(f"{n}.branch3x3_2", y, n, 0, sb)
+    y = conv(f"{n}.branch7x7x3_1", x)
+    y = conv(f"{n}.branch7x7x3_2", y)
+    y = conv(f"{n}.branch7x7x3_3", y)
+    conv(f"{n}.branch7x7x3_4", y, n, 320, sb)
+    pool("max", x, n, 3, 2, 0, off=512)
+    x = n
+
+    def mixed_e(n, x):
+        t = T[x]
+        sb = float(np.float32(block_scale([f"{n}.branch1x1", f"{n}.branch3x3_2a", f"{n}.branch3x3dbl_3a"], x)))
+        T[n] = dict(H=8, W=8, C=2048, zp=0, s=sb)
+        conv(f"{n}.branch1x1", x, n, 0, sb)
+        y = conv(f"{n}.branch3x3_1", x)
+        conv(f"{n}.branch3x3_2a", y, n, 320, sb)
+        conv(f"{n}.branch3x3_2b", y, n, 704, sb)
+        y = conv(f"{n}.branch3x3dbl_1", x)
+        y = conv(f"{n}.branch3x3dbl_2", y)
+        conv(f"{n}.branch3x3dbl_3a", y, n, 1088, sb)
+        conv(f"{n}.branch3x3dbl_3b", y, n, 1472, sb)
+        y = pool("avg", x, f"{n}.pool", 3, 1, 1)
+        conv(f"{n}.branch_pool", y, n, 1856, sb)
+        return n
+
+    x = mixed_e("Mixed_7b", x)
+    x = mixed_e("Mixed_7c", x)
+    assert len(layers) == 94
+    gap = pool("avg", x, "gap", 8, 1, 0)
+    g = gen.rng(seed + 99)
+    fc = dict(zp_A=T[gap]["zp"], s_A=T[gap]["s"], W=gen.rand_q(g, (1000, 2048), "s8", -127, 127),
+              s_W=g.uniform(0.002, 0.02, size=1000).astype(np.float32),
+              bias=g.integers(-4096, 4097, size=1000).astype(np.int32))
+    image = gen.rng(seed + 98).standard_normal((batch, 299, 299, 3)).astype(np.float32)
+    return dict(layers=layers, ops=ops, tensors=T, fc=fc, image=image, img_scale=img_scale, img_zp=img_zp,
+                batch=batch, out="gap")
+
+
+def shard_inception(m, lo: int, hi: int):
+    return dict(m, image=m["image"][lo:hi], batch=hi - lo)
+
+
+class GpuInceptionV3:
+    """The Inception-v3 forward on the library's ops (branch convs write into channel slices of
+    the concat buffers), captured as one CUDA graph."""
+
+    def __init__(self, m, dev):
+        import torch
+
+        from paper_2006_10226_b200 import qnn
+        self.torch, self.qnn, self.m = torch, qnn, m
+        B = m["batch"]
+        T = m["tensors"]
+        self.buf = {name: torch.empty((B, t["H"], t["W"], t["C"]), dtype=torch.uint8, device=dev)
+                    for name, t in T.items() if name != "image"}
+        self.ops = {}
+        for name, L in m["layers"].items():
+            c = L["c"]
+            dst = [o for o in m["ops"] if o.get("name") == name][0]["dst"]
+            ocs = T[dst]["C"] if dst != name else 0
+            self.ops[name] = qnn.PackedConv2d(B, c.H, c.W, c.C, torch.from_numpy(L["W"]).to(dev),
+                                              torch.from_numpy(L["bias"]).to(dev), L["zp_A"], 0, L["s_A"], L["s_W"],
+                                              L["out"], c.stride, c.pad, (1, 1), 1, out_cstride=ocs)
+        self.image_d = torch.from_numpy(m["image"]).to(dev)
+        self.buf["image"] = torch.empty(self.image_d.shape, dtype=torch.uint8, device=dev)
+        fc = m["fc"]
+        self.fc = qnn.PackedDense(B, torch.from_numpy(fc["W"]).to(dev), torch.from_numpy(fc["bias"]).to(dev),
+                                  fc["zp_A"], 0, fc["s_A"], fc["s_W"], None)
+        self.fc_out = torch.empty((B, 1000), dtype=torch.int32, device=dev)
+        self.logit_scale = (np.float32(fc["s_A"]) * fc["s_W"].astype(np.float32)).astype(np.float32)
+        self.logits = torch.empty(self.fc_out.shape, dtype=torch.float32, device=dev)
+        self.graph = None
+
+    def step(self):
+        q, m = self.qnn, self.m
+        q.qnn_quantize(self.image_d, [m["img_scale"]], [m["img_zp"]], "u8", out=self.buf["image"])
+        for o in m["ops"]:
+            if o["kind"] == "conv":
+                self.ops[o["name"]](self.buf[o["src"]], out=self.buf[o["dst"]], out_channel_offset=o["off"])
+            else:
+                p = o["pad"]
+                q.qnn_pool2d(self.buf[o["src"]], o["kind"], o["R"], o["R"], (o["stride"],) * 2, (p, p, p, p),
+                             out=self.buf[o["dst"]], out_channel_offset=o["off"])
+        g = self.buf[m["out"]]
+        self.fc(g.view(g.shape[0], -1), out=self.fc_out)
+        q.qnn_dequantize(self.fc_out, self.logit_scale, [0], axis=-1, out=self.logits)
+
+    def capture(self):
+        torch = self.torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        self.qnn.launch_counter_reset()
+        with torch.cuda.graph(self.graph):
+            self.step()
+        self.launches_per_step = self.qnn.launch_counter()
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.graph.replay()
+
+    def total_macs(self):
+        return sum(L["c"].macs(self.m["batch"]) for L in self.m["layers"].values()) + self.m["batch"] * 2048 * 1000
+
+
+def oracle_inception_forward(m, n_img: int = 1, with_buffers: bool = False):
+    """The oracle on the Inception-v3 forward of inception_v3_full_model (NHWC between ops)."""
+    import oracle as orc
+    nchw = lambda t: np.ascontiguousarray(t.transpose(0, 3, 1, 2))
+    nhwc = lambda t: np.ascontiguousarray(t.transpose(0, 2, 3, 1))
+    T = m["tensors"]
+    buf = {"image": orc.quantize(m["image"][:n_img], [m["img_scale"]], [m["img_zp"]], "u8")}
+    for name, t in T.items():
+        if name != "image":
+            buf[name] = np.zeros((n_img, t["H"], t["W"], t["C"]), np.uint8)
+    for o in m["ops"]:
+        x = buf[o["src"]]
+        if o["kind"] == "conv":
+            L = m["layers"][o["name"]]
+            c = L["c"]
+            y = nhwc(orc.qnn_conv2d(nchw(x), nchw(L["W"]), L["zp_A"], 0, L["s_A"], L["s_W"], L["bias"], L["out"],
+                                    c.stride, c.pad))
+        else:
+            p = o["pad"]
+            y = nhwc(orc.pool2d(nchw(x), o["kind"], o["R"], o["R"], (o["stride"],) * 2, (p, p, p, p)))
+        buf[o["dst"]][..., o["off"]:o["off"] + y.shape[-1]] = y
+    g = buf[m["out"]]
+    fc = m["fc"]
+    acc = orc.qnn_dense(g.reshape(g.shape[0], -1), fc["W"], fc["zp_A"], 0, fc["s_A"], fc["s_W"], fc["bias"], None)
+    scale = (np.float32(fc["s_A"]) * fc["s_W"]).astype(np.float32)
+    if with_buffers:
+        return orc.dequantize(acc, scale, [0], axis=-1), acc, buf
+    return orc.dequantize(acc, scale, [0], axis=-1)
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
@@ -503,6 +772,8 @@ def main():
     ap.add_argument("--no-full-network", dest="full_network", action="store_false",
                     help="skip the full-forward (glue ops) measurement")
     ap.add_argument("--no-weak", dest="weak", action="store_false", help="skip the weak-scaling figure (N > 1)")
+    ap.add_argument("--no-inception", dest="inception", action="store_false",
+                    help="skip the Inception-v3 full-forward measurement")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "contract: at least 3 warm-up steps"
 
@@ -697,6 +968,24 @@ def main():
                        "conv3's epilogue), global avg pool, fc, dequantize"}
         del fnet
 
+    # ---------------- Inception-v3 full forward (configs[4]'s second network), same global batch
+    incep = None
+    if args.inception:
+        im = shard_inception(inception_v3_full_model(G), lo, hi)
+        inet = GpuInceptionV3(im, dev)
+        inet.capture()
+        for _ in range(3):
+            inet.replay()
+        torch.cuda.synchronize()
+        isteps = max(3, min(args.steps, 50))
+        ims = _time_replays(torch, inet.replay, isteps, world, dist, dev) / isteps
+        incep = {"value": round(G / (ims / 1000.0), 1), "unit": "images/s", "ms_per_step": round(ims, 4),
+                 "steps": isteps, "launches_per_step": inet.launches_per_step,
+                 "conv_tops": round(2.0 * inet.total_macs() * world / (ims / 1000.0) / 1e12, 1),
+                 "ops": "quantize (299x299x3 f32 -> u8), 94 conv (branch outputs written into channel slices "
+                        "of the concat buffers), 4 max pools, 9 branch avg pools, global avg pool, fc, dequantize"}
+        del inet
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -745,6 +1034,7 @@ def main():
         "cpu_baseline": cpu,
         "weak_scaling": weak,
         "full_network": full,
+        "inception_v3": incep,
         "layers": layers,
     }
     print(json.dumps(line), flush=True)

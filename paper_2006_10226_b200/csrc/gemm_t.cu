@@ -133,6 +133,9 @@ __device__ __forceinline__ int32_t res_term(const GemmTParams& p, uint32_t word,
 struct TChan {
   int32_t M[4], t[4];
   long long k[4];
+  // fused residual (reading R19), UPWARD fast form: R((r - zp_r) * M_r / 2^(32 + rt)) =
+  // hi32((r - zp_r) * M_r + rk) >> rt with rk = 2^(rt - 1) * 2^32 (|r - zp_r| <= 255)
+  int32_t rkh, rt;   // rk = rkh * 2^32
 };
 
 template <int MODE, bool FAST>
@@ -144,7 +147,7 @@ __device__ __forceinline__ int32_t tq1(const TChan& q, int i, uint32_t acc, int3
 
 // 32 of the warp's pixel columns x its quadrant's 32 channels: requantize, (residual), clamp,
 // pack 4 channels per word, store into the staging tile [pixel][32 channels]
-template <int MODE, bool FAST, bool CLAMP, bool S8OUT, bool RES>
+template <int MODE, bool FAST, bool CLAMP, bool S8OUT, bool RES, bool RESFAST = false>
 __device__ __forceinline__ void t_epilogue(const GemmTParams& p, const TChan& q, const uint32_t (&va)[16],
                                            const uint32_t (&vb)[16], uint32_t st0, uint32_t st1, uint32_t rb) {
 #pragma unroll
@@ -162,7 +165,15 @@ __device__ __forceinline__ void t_epilogue(const GemmTParams& p, const TChan& q,
       if (RES) {
         const uint32_t rw = lds32(a);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) y[i] += res_term<MODE>(p, rw, i);
+        for (int i = 0; i < 4; ++i) {
+          if (RESFAST) {
+            const uint32_t b = (rw >> (8 * i)) & 0xFFu;
+            const int32_t x = (p.res_s8 ? (int32_t)(int8_t)b : (int32_t)b) - p.res_zp;
+            y[i] += mad_hi64(x, p.res_M, (long long)q.rkh << 32) >> q.rt;
+          } else {
+            y[i] += res_term<MODE>(p, rw, i);
+          }
+        }
       }
       if (CLAMP || !FAST) {
 #pragma unroll
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   // epilogue warps: the quads holding live channels (all 4, or K_out / 32 in build mode, whose
   // quads 2 and 3 build the X' tiles)
   const int ep_quads = build ? (p.Kout + 31) / 32 : 4;
-  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[4], rawfull[8],
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[8], rawfull[8],
       rawempty[8];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       mbar_init(&tempty[a], 4 * ep_quads);   // 4 column groups x live quads
     }
     mbar_init(&wfull, 1);
-    for (int g = 0; g < 4; ++g) mbar_init(&rbar[g], 1);
+    for (int g = 0; g < 8; ++g) mbar_init(&rbar[g], 1);   // per (group, staging buffer)
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(&tmem_slot, 512);
@@ -466,6 +477,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
         q.k[i] = off;
       }
     }
+    q.rt = 0;
+    q.rkh = 0;
+    if (RES && MODE == 0 && p.res_rsh >= 33 && p.res_rsh <= 52) {
+      q.rt = p.res_rsh - 32;
+      q.rkh = 1 << (q.rt - 1);
+    }
     const int dbg = kTInstrument ? p.dbg : 0;
     const bool all_fast = __all_sync(0xffffffffu, fast);
     // column group grp shares a [kTCols][out_rb] staging tile (1 or 2 buffers) with the other
@@ -489,13 +506,29 @@ __global__ void __launch_bounds__(kTThreads, 1)
       uint8_t* const stage_out = gstage + (nbufs == 2 ? (it & 1) * gbytes : 0);
       const uint32_t sbase = smem_u32(stage_out);
       const int col0 = pt * kTBN + grp * kTCols;
+      // RES: the residual tile (this group's pixels x out_rb channels, same swizzle) lands in the
+      // staging buffer; each thread reads its four channels' word per pixel and overwrites it.
+      // With two buffers it is prefetched one tile ahead (issued while the previous tile
+      // computes), else loaded here.
+      const int b = nbufs == 2 ? (it & 1) : 0;
       if (gleader) {
-        bulk_wait_read_dyn(nbufs - 1);   // the store that last used this buffer has read it
-        if (RES) {
-          // the residual tile (this group's pixels x out_rb channels, same swizzle) lands in the
-          // staging buffer; each thread reads its four channels' word per pixel and overwrites it
-          mbar_arrive_expect_tx(&rbar[grp], gbytes);
-          tma_load_2d(stage_out, &tmR, &rbar[grp], ch * kTBM, col0);
+        if (RES && nbufs == 2) {
+          if (it == 0) {
+            mbar_arrive_expect_tx(&rbar[grp * 2], gbytes);
+            tma_load_2d(stage_out, &tmR, &rbar[grp * 2], ch * kTBM, col0);
+          }
+          if (pt + px_step < npt) {   // next tile's residual into the other buffer
+            bulk_wait_read<0>();      // the store of tile it-1 has read that buffer
+            uint8_t* nb = gstage + (size_t)(b ^ 1) * gbytes;
+            mbar_arrive_expect_tx(&rbar[grp * 2 + (b ^ 1)], gbytes);
+            tma_load_2d(nb, &tmR, &rbar[grp * 2 + (b ^ 1)], ch * kTBM, (pt + px_step) * kTBN + grp * kTCols);
+          }
+        } else {
+          bulk_wait_read_dyn(nbufs - 1);   // the store that last used this buffer has read it
+          if (RES) {
+            mbar_arrive_expect_tx(&rbar[grp * 2], gbytes);
+            tma_load_2d(stage_out, &tmR, &rbar[grp * 2], ch * kTBM, col0);
+          }
         }
       }
       named_bar_sync(1 + grp, 32 * ep_quads);   // the buffer is free for every warp of the group
@@ -503,7 +536,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       tc_fence_after();
       if (warp == 0 && lane == 0) t_trace(p.trace, 320, it);
       const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * kTCols);
-      if (RES) mbar_wait(&rbar[grp], (uint32_t)(it & 1));
+      if (RES) mbar_wait(&rbar[grp * 2 + b], (uint32_t)(nbufs == 2 ? (it >> 1) & 1 : it & 1));
       // all four TMEM loads in flight at once, one wait, and the accumulator handed back to the
       // MMA warp before any math
       uint32_t va0[16], vb0[16], va1[16], vb1[16];
@@ -520,6 +553,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
       if ((dbg & 1) || !quad_live) {
+      } else if (all_fast && RES && q.rt > 0) {   // (q.rt is uniform: one per-tensor residual multiplier)
+        t_epilogue<MODE, true, CLAMP, S8OUT, RES, true>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
+        t_epilogue<MODE, true, CLAMP, S8OUT, RES, true>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
+                                                        sbase + 32 * out_rb + st_off1, out_rb);
       } else if (all_fast) {
         t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
         t_epilogue<MODE, true, CLAMP, S8OUT, RES>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,

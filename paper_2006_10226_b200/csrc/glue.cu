@@ -155,12 +155,135 @@ __global__ void __launch_bounds__(256) pool_kernel(const __grid_constant__ PoolP
   }
 }
 
+// Fast path (16 channels per thread, C % 16 == 0, 16-B aligned pitches): a thread owns TQ
+// consecutive output columns of one output row and one 16-channel group, and loads each input
+// column of their union window once per filter row ((TQ-1)*sw + S loads instead of TQ*S).
+// Max: byte-parallel __vmaxu4 / __vmaxs4.  Average: sums in 16-bit lanes (<= 255 * 128 taps
+// fits; s8 is biased by 128 into u8 and unbiased after), then the rounding division of R20 by
+// an exact multiply-shift: floor(x / d) = (x * (2^32 / d + 1)) >> 32 for x < 2^16, d < 2^8.
+// m = floor(2^32 / d) + 1 is computed once per output (d = 2 * count); x < 2^16 keeps the
+// error x * (m - 2^32 / d) / 2^32 below 1/d, so the floor is exact
+__device__ __forceinline__ uint32_t div_magic(uint32_t d) { return 0xFFFFFFFFu / d + 1u; }
+__device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t m) {
+  return (uint32_t)(((unsigned long long)x * m) >> 32);
+}
+
+template <bool S8, bool AVG, int TQ>
+__global__ void __launch_bounds__(256) pool16_kernel(const __grid_constant__ PoolParams p, FastDiv fdG,
+                                                      FastDiv fdQB, FastDiv fdP) {
+  const int G = p.C >> 4;
+  const int QB = (p.Q + TQ - 1) / TQ;
+  const uint32_t total = (uint32_t)p.N * p.P * QB * G;
+  const uint8_t* in = reinterpret_cast<const uint8_t*>(p.in);
+  uint8_t* out = reinterpret_cast<uint8_t*>(p.out);
+  const uint32_t bias = S8 ? 0x80808080u : 0u;   // s8 -> u8 (x + 128) for the byte-parallel ops
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t rest0 = fdiv(idx, fdG);
+    const int g = (int)(idx - rest0 * G);
+    const uint32_t rest1 = fdiv(rest0, fdQB);
+    const int qb = (int)(rest0 - rest1 * QB);
+    const uint32_t n = fdiv(rest1, fdP);
+    const int pp = (int)(rest1 - n * p.P);
+    const int q0 = qb * TQ;
+    // acc[t][k]: max -> 4 packed bytes per word (4 words = 16 channels); avg -> 2 x 16-bit
+    // lanes per word (8 words: even bytes in [0..3], odd bytes in [4..7])
+    uint32_t acc[TQ][8];
+#pragma unroll
+    for (int t = 0; t < TQ; ++t)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[t][k] = 0u;
+    int rows = 0;
+    const int w0 = q0 * p.sw - p.pl;
+    const int ncols = (TQ - 1) * p.sw + p.S;
+    for (int r = 0; r < p.R; ++r) {
+      const int h = pp * p.sh + r - p.pt;
+      if (h < 0 || h >= p.H) continue;
+      ++rows;
+      const uint8_t* rowp = in + (((long long)n * p.H + h) * p.W) * p.in_cs + g * 16;
+      for (int c = 0; c < ncols; ++c) {
+        const int w = w0 + c;
+        if (w < 0 || w >= p.W) continue;
+        const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(rowp + (long long)w * p.in_cs));
+        const uint32_t v[4] = {v4.x ^ bias, v4.y ^ bias, v4.z ^ bias, v4.w ^ bias};
+#pragma unroll
+        for (int t = 0; t < TQ; ++t) {
+          const int sidx = c - t * p.sw;
+          if (sidx < 0 || sidx >= p.S) continue;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (AVG) {
+              acc[t][k] = __vadd2(acc[t][k], v[k] & 0x00FF00FFu);
+              acc[t][k + 4] = __vadd2(acc[t][k + 4], (v[k] >> 8) & 0x00FF00FFu);
+            } else {
+              acc[t][k] = __vmaxu4(acc[t][k], v[k]);   // (biased s8 orders like u8)
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < TQ; ++t) {
+      const int q = q0 + t;
+      if (q >= p.Q) break;
+      uint32_t ow[4];
+      if (AVG) {
+        int cols = 0;
+        for (int sidx = 0; sidx < p.S; ++sidx) {
+          const int w = q * p.sw + sidx - p.pl;
+          cols += (w >= 0 && w < p.W) ? 1 : 0;
+        }
+        const int cnt = rows * cols;
+        const uint32_t mag = div_magic(2u * (uint32_t)(cnt > 0 ? cnt : 1));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t bytes = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t word = j & 1 ? acc[t][k + 4] : acc[t][k];
+            int32_t sum = (int32_t)((word >> (16 * (j >> 1))) & 0xFFFFu);
+            if (S8) sum -= 128 * cnt;
+            int32_t y = 0;
+            if (cnt > 0) {
+              // sign(s) * floor((2|s| + n) / (2n)): ties away from zero (reading R20)
+              const uint32_t a = (uint32_t)(sum < 0 ? -sum : sum);
+              const int32_t m = (int32_t)div_small(2u * a + (uint32_t)cnt, mag);
+              y = sum < 0 ? -m : m;
+            }
+            bytes |= ((uint32_t)y & 0xFFu) << (8 * j);
+          }
+          ow[k] = bytes;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ow[k] = acc[t][k] ^ bias;
+      }
+      uint8_t* dst = out + (((long long)n * p.P + pp) * p.Q + q) * p.out_cs + g * 16;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+  }
+}
+
 cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool v16 = p.C % 16 == 0 && p.in_cs % 16 == 0 && p.out_cs % 16 == 0 &&
                    ((reinterpret_cast<uintptr_t>(p.in) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
+  // fast path: every window has a valid tap (pad < window, checked by the ABI), sums of at
+  // most 128 taps fit the 16-bit lanes, and the work-item count fits 32 bits
+  constexpr int kTQ = 4;
+  const long long items = (long long)p.N * p.P * ((p.Q + kTQ - 1) / kTQ) * (p.C / 16);
+  if (v16 && p.R * p.S <= 128 && items < (1ll << 31)) {
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, (long long)sms * 16));
+    const FastDiv fdG = make_fastdiv((uint32_t)(p.C / 16)), fdQB = make_fastdiv((uint32_t)((p.Q + kTQ - 1) / kTQ)),
+                  fdP = make_fastdiv((uint32_t)p.P);
+#define QNN_POOL16(S_, A_) \
+  if (p.s8 == S_ && p.avg == A_) pool16_kernel<S_, A_, kTQ><<<blocks, 256, 0, s>>>(p, fdG, fdQB, fdP);
+    QNN_POOL16(false, false) QNN_POOL16(false, true) QNN_POOL16(true, false) QNN_POOL16(true, true)
+#undef QNN_POOL16
+    count_launch();
+    return cudaGetLastError();
+  }
   const long long total = (long long)p.N * p.P * p.Q * (v16 ? p.C / 16 : p.C);
   const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)sms * 16));
 #define QNN_POOL(V_, S_, A_) \

@@ -221,14 +221,22 @@ class PackedConv2d:
         d = self.desc
         return (d.N, self.P, self.Q, d.out_cstride or self.K)
 
-    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None, residual=None) -> torch.Tensor:
-        """Run the conv; residual=(tensor NHWC, scale, zero_point) fuses a qnn.add of it (reading R19)."""
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None, residual=None,
+                 out_channel_offset: int = 0) -> torch.Tensor:
+        """Run the conv; residual=(tensor NHWC, scale, zero_point) fuses a qnn.add of it (reading R19).
+        With out_cstride set at construction, ``out`` may be a wider NHWC buffer (e.g. an Inception
+        concat) and the conv writes channels [out_channel_offset, + K) of every pixel."""
         if out is None:
             out = torch.empty(self.out_shape(), dtype=self.out_dtype, device=x.device)
+        optr = _dev(out, "out")
+        if out_channel_offset:
+            if not self.desc.out_cstride or out.shape[-1] != self.desc.out_cstride:
+                raise QnnError("out_channel_offset needs out_cstride == out.shape[-1]")
+            optr = ctypes.c_void_p(optr.value + int(out_channel_offset) * out.element_size())
         ws = ctypes.c_void_p(self.workspace.data_ptr()) if self.workspace is not None else None
         if residual is None:
             _check(lib().qnn_conv2d_packed(ctypes.byref(self.desc), self._op, ctypes.c_void_p(self.packed.data_ptr()),
-                                           _dev(x, "x"), _dev(out, "out"), ws, self.ws_bytes,
+                                           _dev(x, "x"), optr, ws, self.ws_bytes,
                                            ctypes.c_void_p(_stream(stream))), "qnn_conv2d_packed")
         else:
             r, rs, rz = residual
@@ -376,15 +384,19 @@ def qnn_add(a: torch.Tensor, s_a: float, zp_a: int, b: torch.Tensor, s_b: float,
 
 
 def qnn_pool2d(x: torch.Tensor, mode: str, R: int, S: int, stride=(1, 1), pad=(0, 0, 0, 0), out=None,
-               stream=None) -> torch.Tensor:
-    """Max / average pooling of an NHWC 8-bit tensor (padding excluded, reading R20)."""
+               stream=None, out_channel_offset: int = 0) -> torch.Tensor:
+    """Max / average pooling of an NHWC 8-bit tensor (padding excluded, reading R20).  ``out`` may
+    be wider than x (a concat buffer): the result goes to channels [out_channel_offset, + C)."""
     N, H, W, C = x.shape
-    d = Pool2dDesc(N, H, W, C, R, S, stride[0], stride[1], pad[0], pad[1], pad[2], pad[3], 0, 0,
-                   _TORCH_DT[x.dtype], 0 if mode == "max" else 1)
     P = (H + pad[0] + pad[2] - R) // stride[0] + 1
     Q = (W + pad[1] + pad[3] - S) // stride[1] + 1
     if out is None:
         out = torch.empty((N, P, Q, C), dtype=x.dtype, device=x.device)
-    _check(lib().qnn_pool2d(ctypes.byref(d), _dev(x, "x"), _dev(out, "out"), ctypes.c_void_p(_stream(stream))),
-           "qnn_pool2d")
+    ocs = out.shape[-1] if out.shape[-1] != C or out_channel_offset else 0
+    d = Pool2dDesc(N, H, W, C, R, S, stride[0], stride[1], pad[0], pad[1], pad[2], pad[3], 0, ocs,
+                   _TORCH_DT[x.dtype], 0 if mode == "max" else 1)
+    optr = _dev(out, "out")
+    if out_channel_offset:
+        optr = ctypes.c_void_p(optr.value + int(out_channel_offset) * out.element_size())
+    _check(lib().qnn_pool2d(ctypes.byref(d), _dev(x, "x"), optr, ctypes.c_void_p(_stream(stream))), "qnn_pool2d")
     return out

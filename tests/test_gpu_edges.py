@@ -119,3 +119,59 @@ def test_pixel_major_generic_path_large_bias(mode):
     _, _, y = gpu_conv(case)
     got, want = y.cpu().numpy(), oracle_conv(case)
     assert np.array_equal(got, want), mismatch_report(got, want)
+
+
+def _guarded(shape, dtype, guard=4096, fill=0xA5):
+    """An output view inside a larger buffer whose guard bytes (before, after) hold `fill`."""
+    n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+    raw = torch.full((guard + n + guard,), fill, dtype=torch.uint8, device="cuda")
+    view = raw[guard:guard + n].view(dtype).view(shape)
+    return raw, view
+
+
+@pytest.mark.parametrize("kind", ["pointwise_t", "rows3x3", "stem_build", "im2col", "depthwise", "dense_raw",
+                                  "channel_slice"])
+def test_no_writes_outside_the_output(kind):
+    """compute-sanitizer is closed on this pool, so out-of-bounds WRITES are checked directly:
+    every kernel family writes into a view of a buffer with 4 KB guard zones on both sides (and,
+    for a channel-strided output, into every other channel slice), which must stay untouched."""
+    from paper_2006_10226_b200 import PackedConv2d, PackedDense
+    from gpu_helpers import to_dev
+    cases = {
+        "pointwise_t": gen.conv_case(7401, 2, 64, 9, 7, 256, 1, 1),
+        "rows3x3": gen.conv_case(7402, 1, 64, 11, 9, 64, 3, 3, (1, 1), (1, 1, 1, 1)),
+        "stem_build": gen.conv_case(7403, 2, 3, 30, 30, 64, 7, 7, (2, 2), (3, 3, 3, 3)),
+        "im2col": gen.conv_case(7404, 2, 96, 9, 9, 130, 3, 3, (2, 2), (1, 1, 1, 1)),
+        "depthwise": gen.conv_case(7405, 2, 48, 9, 10, 48, 3, 3, (1, 1), (1, 1, 1, 1), (1, 1), 48),
+        "channel_slice": gen.conv_case(7406, 2, 64, 8, 8, 128, 1, 1),
+    }
+    if kind == "dense_raw":
+        d = gen.dense_case(7407, 100, 300, 512, out_dtype="s32")
+        op = PackedDense(100, to_dev(d.W), to_dev(d.bias), d.zp_A, d.zp_W, d.s_A, d.s_W, None)
+        raw, y = _guarded((100, 300), torch.int32)
+        op(to_dev(d.A), out=y)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), orc.qnn_dense(d.A, d.W, d.zp_A, d.zp_W, d.s_A, d.s_W, d.bias, None))
+    else:
+        c = cases[kind]
+        N, H, W, C = c.A.shape
+        wide = kind == "channel_slice"
+        K = c.W.shape[0]
+        op = PackedConv2d(N, H, W, C, to_dev(c.W), to_dev(c.bias), c.zp_A, c.zp_W, c.s_A, c.s_W, c.out_params(),
+                          c.stride, c.pad, c.dil, c.groups, out_cstride=3 * K if wide else 0)
+        oshape = op.out_shape()
+        raw, y = _guarded(oshape, torch.uint8)
+        if wide:
+            op(to_dev(c.A), out=y, out_channel_offset=K)
+        else:
+            op(to_dev(c.A), out=y)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        want = oracle_conv(c)
+        if wide:
+            assert np.array_equal(got[..., K:2 * K], want)
+            assert (got[..., :K] == 0xA5).all() and (got[..., 2 * K:] == 0xA5).all()
+        else:
+            assert np.array_equal(got, want)
+    r = raw.cpu().numpy()
+    assert (r[:4096] == 0xA5).all() and (r[-4096:] == 0xA5).all(), "write outside the output"

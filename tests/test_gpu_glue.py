@@ -57,6 +57,19 @@ POOLS = [
 ]
 
 
+POOLS += [
+    # the fast 16-channel kernel at network shapes (ragged Q vs its 4-column blocks), both dtypes
+    (2, 35, 35, 256, 3, 3, (1, 1), (1, 1, 1, 1), "avg", "u8"),     # Inception branch avg pool
+    (2, 35, 35, 48, 3, 3, (1, 1), (1, 1, 1, 1), "avg", "s8"),
+    (2, 147, 147, 64, 3, 3, (2, 2), (0, 0, 0, 0), "max", "u8"),    # Inception stem max pool
+    (2, 112, 112, 64, 3, 3, (2, 2), (1, 1, 1, 1), "max", "s8"),    # ResNet-50 stem max pool
+    (3, 8, 8, 2048, 8, 8, (1, 1), (0, 0, 0, 0), "avg", "u8"),      # Inception global avg pool
+    (3, 7, 7, 2048, 7, 7, (1, 1), (0, 0, 0, 0), "avg", "s8"),      # ResNet-50 global avg pool
+    (1, 17, 13, 32, 5, 3, (2, 1), (2, 1, 1, 0), "avg", "u8"),      # asymmetric everything
+    (1, 9, 11, 16, 11, 11, (1, 1), (5, 5, 5, 5), "avg", "s8"),     # 121 taps: the 16-bit lane limit side
+]
+
+
 @pytest.mark.parametrize("cfg", POOLS, ids=lambda c: f"{c[8]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}{c[5]}")
 def test_pool(q, cfg):
     N, H, W, C, R, S, st, pad, mode, dt = cfg
@@ -99,3 +112,16 @@ def test_conv_fused_residual_add(q, cfg):
                               np.ascontiguousarray(res.transpose(0, 3, 1, 2)), s_res, zp_res, case.out_params(),
                               case.stride, case.pad).transpose(0, 2, 3, 1)
     assert np.array_equal(y, want), (np.argwhere(y != want)[:5], y.size)
+
+
+def test_pool_into_channel_slice(q):
+    """Pooling written into channels [96, 96 + C) of a wider concat buffer (Inception reduction
+    blocks); the other channels stay untouched."""
+    g = np.random.default_rng(77)
+    x = gen.rand_q(g, (2, 17, 17, 64), "u8")
+    want = orc.pool2d(np.ascontiguousarray(x.transpose(0, 3, 1, 2)), "max", 3, 3, (2, 2)).transpose(0, 2, 3, 1)
+    buf = torch.full((2, 8, 8, 256), 7, dtype=torch.uint8, device="cuda")
+    q.qnn_pool2d(torch.from_numpy(x).cuda(), "max", 3, 3, (2, 2), out=buf, out_channel_offset=96)
+    b = buf.cpu().numpy()
+    assert np.array_equal(b[..., 96:160], want)
+    assert (b[..., :96] == 7).all() and (b[..., 160:] == 7).all()

@@ -68,3 +68,45 @@ def test_bench_shards_concatenate_to_one_gpu_output(world):
         torch.cuda.synchronize()
         parts.append(n.logits.cpu().numpy())
     assert np.array_equal(np.concatenate(parts).view(np.int32), ffull.logits.cpu().numpy().view(np.int32))
+
+
+def test_inception_v3_full_forward_matches_oracle():
+    """configs[4]'s second network as a true forward: 94 convs whose branch
+    outputs land in channel slices of the concat buffers (out_cstride), stem and reduction max
+    pools, branch average pools, global average pool, fc, dequantize -- bit-exact logits, and
+    every intermediate buffer equal, vs the oracle running the same ops one by one."""
+    import bench
+    m = bench.inception_v3_full_model(2, seed=7100)
+    net = bench.GpuInceptionV3(m, torch.device("cuda"))
+    for b in net.buf.values():
+        b.fill_(0xA5)                     # sentinel: a channel slice left unwritten shows up below
+    net.step()
+    torch.cuda.synchronize()
+    want_logits, want_acc, want_buf = bench.oracle_inception_forward(m, 2, with_buffers=True)
+    for name, b in want_buf.items():
+        assert np.array_equal(net.buf[name].cpu().numpy(), b), name
+    assert np.array_equal(net.fc_out.cpu().numpy(), want_acc.astype(np.int32))
+    got = net.logits.cpu().numpy()
+    # int32 -> fp32 dequantize: BJ:north_star allows 1 ulp (fl32(s * fl32(q - zp)) rounds twice)
+    ulps = np.abs(got.view(np.int32).astype(np.int64) - want_logits.view(np.int32).astype(np.int64))
+    assert ulps.max() <= 1
+    assert np.unique(got).size > 100 and not np.array_equal(got[0], got[1])
+
+
+def test_inception_v3_shards_concatenate():
+    import bench
+    from paper_2006_10226_b200.sharding import shard_range
+    G, world = 6, 2
+    m = bench.inception_v3_full_model(G, seed=7200)
+    dev = torch.device("cuda")
+    full = bench.GpuInceptionV3(m, dev)
+    full.step()
+    torch.cuda.synchronize()
+    parts = []
+    for r in range(world):
+        lo, hi = shard_range(G, r, world)
+        n = bench.GpuInceptionV3(bench.shard_inception(m, lo, hi), dev)
+        n.step()
+        torch.cuda.synchronize()
+        parts.append(n.logits.cpu().numpy())
+    assert np.array_equal(np.concatenate(parts).view(np.int32), full.logits.cpu().numpy().view(np.int32))

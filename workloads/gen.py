@@ -43,6 +43,18 @@ def calibrated_out_scale(kk: int, a_range, zp_A: int, w_range, zp_W: int, s_A: f
     return float(np.float32(sigmas * sd * s_A * s_W / out_levels))
 
 
+def calibrated_out_scale_var(kk: int, var_a: float, var_w: float, s_A: float, s_W: float,
+                             out_levels: float = 255.0, sigmas: float = 6.0) -> float:
+    """As calibrated_out_scale, from the second moments of the zero-point-subtracted input and
+    weight codes (e.g. a post-ReLU activation calibrated to 6 sigma over 255 levels has
+    E[a^2] = (255/6)^2 / 2 ~ 903, not the uniform distribution's ~21675)."""
+    sd = math.sqrt(kk * var_a * var_w)
+    return float(np.float32(sigmas * sd * s_A * s_W / out_levels))
+
+
+POST_RELU_VAR = (255.0 / 6.0) ** 2 / 2.0      # E[y^2] of max(0, N(0, s)) coded at 6 s / 255 per level
+
+
 @dataclass
 class ConvCase:
     """One qnn.conv2d problem in the kernels' NHWC / OHWI layout."""
