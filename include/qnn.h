@@ -102,10 +102,18 @@ typedef struct {
   qnn_dtype_t input_dtype;     /* QNN_U8 or QNN_S8                                      */
   qnn_dtype_t kernel_dtype;    /* QNN_U8 or QNN_S8                                      */
   int32_t input_zero_point;    /* zp_A                                                   */
-  int32_t kernel_zero_point;   /* zp_W, scalar (per-channel weight zp unsupported, R11) */
+  int32_t kernel_zero_point;   /* zp_W, per-tensor (used when num_kernel_zero_points == 0) */
   float input_scale;           /* s_A                                                    */
   const float* kernel_scales;  /* host; 1 (per-tensor) or K (per-channel, axis 0) values*/
   int32_t num_kernel_scales;
+  /* Per-channel weight zero points (the paper discusses per-channel
+   * scales only, P:37, P:227 -- reading R11 extends Eq. 3 channel by channel):
+   * host array of K values in the kernel dtype's range, or NULL with count 0.  Term 3 is
+   * then zp_W[k] * rowsum, folded into the contraction (weights packed as W - zp_W[k],
+   * split into two s8 k-blocks); channels whose W - zp_W[k] range is not inside
+   * [-256, 254] (s8 weights with zp_W[k] = -128) give QNN_ERR_UNSUPPORTED. */
+  const int32_t* kernel_zero_points;
+  int32_t num_kernel_zero_points;   /* 0 (use kernel_zero_point) or K                      */
 } qnn_conv2d_desc_t;
 
 /* Quantized dense (qnn.dense; "matmul"): out[m,n] over A (M x K) and
@@ -119,6 +127,8 @@ typedef struct {
   float s_A;
   const float* s_W;            /* host; 1 or N values                                   */
   int32_t n_sW;
+  const int32_t* zp_Ws;        /* host; per-output-channel weight zero points (N values), or NULL */
+  int32_t n_zpW;               /* 0 (use zp_W) or N                                     */
 } qnn_dense_desc_t;
 
 QNN_API const char* qnn_status_string(qnn_status_t status);

@@ -142,8 +142,27 @@ def _conv_common(A, Wt, stride, pad, dil, groups):
     return A, Wt, args, out_hw(H, W, R, S, stride, pad, dil)
 
 
+def _per_channel(zp_W):
+    """A per-output-channel weight zero-point vector, or None for a scalar."""
+    z = np.asarray(zp_W)
+    return None if z.ndim == 0 else z.astype(np.int64).reshape(-1)
+
+
 def conv2d_acc(A, Wt, zp_A, zp_W, bias=None, stride=(1, 1), pad=(0, 0, 0, 0), dil=(1, 1), groups=1):
-    """int64 acc[n,k,p,q] = sum (a - zp_A)(W - zp_W) + bias[k]; a = zp_A when padded."""
+    """int64 acc[n,k,p,q] = sum (a - zp_A)(W - zp_W) + bias[k]; a = zp_A when padded.
+    zp_W may be one value per output channel k (f4): Eq. 2 then holds channel by channel, so the
+    result is assembled from one scalar-zp_W evaluation per channel (for groups == C, the
+    channel's own input plane)."""
+    zv = _per_channel(zp_W)
+    if zv is not None:
+        K = Wt.shape[0]
+        assert zv.size == K and groups in (1, A.shape[1])
+        parts = []
+        for k in range(K):
+            Ak = A[:, k:k + 1] if groups > 1 else A
+            bk = None if bias is None else np.asarray(bias)[k:k + 1]
+            parts.append(conv2d_acc(Ak, Wt[k:k + 1], zp_A, int(zv[k]), bk, stride, pad, dil, 1))
+        return np.concatenate(parts, axis=1)
     A, Wt, args, (P, Q) = _conv_common(A, Wt, stride, pad, dil, groups)
     b = None if bias is None else np.ascontiguousarray(bias, dtype=np.int32)
     out = np.zeros((A.shape[0], Wt.shape[0], P, Q), np.int64)
@@ -171,7 +190,12 @@ def conv2d_eq3(A, Wt, zp_A, zp_W, bias=None, stride=(1, 1), pad=(0, 0, 0, 0), di
 
 
 def dense_acc(A, Wt, zp_A, zp_W, bias=None):
-    """int64 acc[m,n] = sum_k (A[m,k] - zp_A)(W[n,k] - zp_W) + bias[n]."""
+    """int64 acc[m,n] = sum_k (A[m,k] - zp_A)(W[n,k] - zp_W) + bias[n] (zp_W scalar or per n)."""
+    zv = _per_channel(zp_W)
+    if zv is not None:
+        return np.concatenate([dense_acc(A, Wt[n:n + 1], zp_A, int(zv[n]),
+                                         None if bias is None else np.asarray(bias)[n:n + 1])
+                               for n in range(Wt.shape[0])], axis=1)
     A = np.ascontiguousarray(A)
     Wt = np.ascontiguousarray(Wt)
     M, K = A.shape

@@ -203,6 +203,11 @@ struct ConvPlan {
   // channel-major GEMM (gemm_t.cu) for wide pointwise layers: chosen at plan time (its weights
   // are packed in the perm32 lane order as a second copy, pk_wt); at run time it also needs a
   // 16-B aligned output, else the pixel-major kernel runs on pk_w
+  // weight zero points: per-channel vector (f4) or the scalar repeated; wsplit: Term 3 folded
+  // into the contraction (weights packed as W - zp_W[k] in two s8 parts), else row sums
+  std::vector<int32_t> zpv;
+  bool zp_vec = false, any_zpw = false, wsplit = false;
+  size_t pk_zpv = 0;
   bool trans = false, t_wres = false;
   int t_stages = 0, t_Kt = 0, t_bufs = 1;
   // channel-major build mode (small-C stems with K_out <= 64): X' built in smem by the idle quads
@@ -287,6 +292,17 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   if (!zp_ok(d->input_dtype, d->input_zero_point) || !zp_ok(d->kernel_dtype, d->kernel_zero_point))
     return QNN_ERR_INVALID_VALUE;
   if (d->C % d->groups != 0 || d->K % d->groups != 0) return QNN_ERR_INVALID_VALUE;
+  // weight zero points: scalar, or one per output channel (f4; reading R11)
+  if (d->num_kernel_zero_points != 0) {
+    if (d->num_kernel_zero_points != d->K || !d->kernel_zero_points) return QNN_ERR_INVALID_VALUE;
+    pl.zp_vec = true;
+    pl.zpv.assign(d->kernel_zero_points, d->kernel_zero_points + d->K);
+    for (int32_t z : pl.zpv)
+      if (!zp_ok(d->kernel_dtype, z)) return QNN_ERR_INVALID_VALUE;
+  } else {
+    pl.zpv.assign(d->K, d->kernel_zero_point);
+  }
+  for (int32_t z : pl.zpv) pl.any_zpw |= z != 0;
   pl.depthwise = d->groups > 1;
   if (pl.depthwise && !(d->groups == d->C && d->K == d->C)) return QNN_ERR_UNSUPPORTED;
   const long long Pn = ((long long)d->H + d->pad_t + d->pad_b - (long long)d->dil_h * (d->R - 1) - 1) / d->stride_h + 1;
@@ -326,7 +342,11 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     pl.pk_rsh = off;
     off = align256(off + (size_t)(C + 31) / 32 * 32 * 4);
     // tensor-core path (depthwise_tc.cu): diagonal B tiles, per-border-class folded offsets
-    pl.dwtc = C % 16 == 0 && d->kernel_dtype == QNN_S8 && d->kernel_zero_point == 0 && d->dil_h == 1 &&
+    if (pl.zp_vec) {
+      pl.pk_zpv = off;
+      off = align256(off + (size_t)C * 4);
+    }
+    pl.dwtc = C % 16 == 0 && d->kernel_dtype == QNN_S8 && !pl.any_zpw && d->dil_h == 1 &&
               d->dil_w == 1 && (d->stride_h == 1 || d->stride_h == 2) && (d->stride_w == 1 || d->stride_w == 2) &&
               pl.in_cs % 16 == 0 && pl.out_cs % 16 == 0;
     if (pl.dwtc) {
@@ -428,19 +448,39 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   if (st != QNN_OK) return st;
   if (pl.ct.ncr * pl.ct.ncc > 255) return QNN_ERR_UNSUPPORTED;
   {
+    // Term 3 (zp_W != 0) folded into the contraction when every channel's W - zp_W[k] range fits
+    // two s8 parts ([-256, 254]: all u8 weights with zp >= 1, s8 weights with zp >= -127) and
+    // the input is not width-folded; else the row-sum pass (scalar zp_W only).  QNN_NO_WSPLIT=1
+    // keeps the row sums for a scalar zp_W (A/B measurements).
+    // A scalar zp_W on a long reduction (KK >= 2048: the tensor-core-bound 3x3 layers, where
+    // doubling the MMAs costs more than the row-sum pass; measured on ResNet-50 b256) keeps
+    // the row sums.  (A width-folded input must also be built in smem: checked below.)
+    static const bool no_wsplit = std::getenv("QNN_NO_WSPLIT") != nullptr;
+    int64_t wlo, whi;
+    dtype_range(d->kernel_dtype, &wlo, &whi);
+    bool splittable = true;
+    for (int32_t z : pl.zpv) splittable &= wlo - z >= -256 && whi - z <= 254;
+    const long long KKs = (long long)(d->C / d->groups) * d->R * d->S;
+    pl.wsplit = pl.any_zpw && splittable && (pl.zp_vec || (!no_wsplit && KKs < 2048));
+    if (pl.zp_vec && pl.any_zpw && !pl.wsplit) return QNN_ERR_UNSUPPORTED;
+  }
+  const int bparts = pl.wsplit ? 2 : 1;
+  {
     const int ncls = pl.ct.ncr * pl.ct.ncc;
     const int num_kb = d->R * pl.gS * pl.nchunks;
     // keep the whole weight operand resident when it is one N tile and leaves room for >= 4 A stages
     pl.b_res_kb = 0;
     // (several N tiles: each CTA keeps one, see the grid above)
     const bool one_n = pl.num_n == 1 || pl.grid % pl.num_n == 0;
-    if (one_n && gemm_smem_bytes(pl.BK, pl.BN, 4, ncls, num_kb, 1) <= 227 * 1024) pl.b_res_kb = num_kb;
+    if (one_n && gemm_smem_bytes(pl.BK, pl.BN, 4, ncls, num_kb * bparts, 1, 0, 0, bparts) <= 227 * 1024)
+      pl.b_res_kb = num_kb;
     // k-blocks per stage: about 32 KB of operands per barrier round trip, at least 3 stages
-    const int per_kb = kGemmBM * pl.BK + (pl.b_res_kb ? 0 : pl.BN * pl.BK);
+    const int per_kb = kGemmBM * pl.BK + (pl.b_res_kb ? 0 : pl.BN * pl.BK * bparts);
     pl.kps = std::max(1, std::min(num_kb, 32768 / per_kb));
-    while (pl.kps > 1 && gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, pl.kps) < 3) --pl.kps;
-    pl.stages = gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, pl.kps);
-    if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, ncls, pl.b_res_kb, pl.kps) > 227 * 1024) return QNN_ERR_UNSUPPORTED;
+    while (pl.kps > 1 && gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb * bparts, pl.kps, 0, 0, bparts) < 3) --pl.kps;
+    pl.stages = gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb * bparts, pl.kps, 0, 0, bparts);
+    if (gemm_smem_bytes(pl.BK, pl.BN, pl.stages, ncls, pl.b_res_kb * bparts, pl.kps, 0, 0, bparts) > 227 * 1024)
+      return QNN_ERR_UNSUPPORTED;
   }
 
   // fold with one 32-byte k-block per filter row, resident weights and contiguous rows: the GEMM
@@ -473,7 +513,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
         pl.stages = st;
       }
     }
-    if (pl.a_build && d->kernel_zero_point == 0) {
+    if (pl.a_build && (!pl.any_zpw || pl.wsplit)) {
       // the builders write zp_A (not 0) outside the image, so every tap is valid: one border
       // class, off = bias - zp_A * sum_taps W, and a per-class-free epilogue (zp_W == 0: no row sums)
       pl.a_zpfill = true;
@@ -484,6 +524,10 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       pl.colcls.assign(pl.Q, 0);
       pl.stages = gemm_max_stages(pl.BK, pl.BN, 1, pl.b_res_kb, pl.kps, pl.a_raw_bytes);
     }
+  }
+  if (pl.wsplit && pl.fold && !pl.a_build) {   // the HBM width-fold path keeps the row sums
+    if (pl.zp_vec) return QNN_ERR_UNSUPPORTED;
+    pl.wsplit = false;
   }
   // a_rows: stride-1 im2col convs with resident weights load the input rows a tile touches
   // once per channel chunk and address every tap through the MMA descriptor (no per-tap
@@ -503,8 +547,9 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     const int ncls = pl.ct.ncr * pl.ct.ncc;
     const int num_kb = d->R * d->S * pl.nchunks;
     if (Wp <= 256 && nri <= 256 && a_stage <= 96 * 1024) {
-      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb, d->R * d->S, 0, (int)a_stage);
-      if (st >= 2 && gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb, d->R * d->S, 0, (int)a_stage) <= 227 * 1024) {
+      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts);
+      if (st >= 2 &&
+          gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts) <= 227 * 1024) {
         pl.a_rows = true;
         pl.a_Wp = Wp;
         pl.a_T = T;
@@ -525,7 +570,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
     static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
     if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows && d->groups == 1 &&
-        d->kernel_zero_point == 0 && d->kernel_dtype == QNN_S8 && pl.requant &&
+        (!pl.any_zpw || pl.wsplit) && (d->kernel_dtype == QNN_S8 || pl.wsplit) && pl.requant &&
         (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
         pl.out_cs % 16 == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
       const int num_kb = pl.nchunks;   // one tap
@@ -535,8 +580,9 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       for (const auto& o : opts) {
         const int bufs = o[0];
         const bool w_res = o[1] != 0;
-        const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res, bufs);
-        if (stages >= (bufs == 2 ? 4 : 3) && gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res, bufs) <= 226 * 1024) {
+        const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res, bufs, -1, 0, 128, bparts);
+        if (stages >= (bufs == 2 ? 4 : 3) &&
+            gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res, bufs, -1, 0, 128, bparts) <= 226 * 1024) {
           pl.trans = true;
           pl.t_wres = w_res;
           pl.t_stages = stages;
@@ -556,8 +602,8 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     static const bool no_tbuild = std::getenv("QNN_NO_TBUILD") != nullptr;
     const long long rowlen = (long long)d->W * d->C;
     if (!no_tbuild && pl.a_build && pl.a_zpfill && d->K <= 64 && d->K % 32 == 0 && d->dil_h == 1 &&
-        d->kernel_dtype == QNN_S8 && (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && pl.out_cs % 16 == 0 &&
-        d->R <= 16) {
+        (d->kernel_dtype == QNN_S8 || pl.wsplit) && (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) &&
+        pl.out_cs % 16 == 0 && d->R <= 16) {
       int ib = 0;
       for (int c : {256, 128, 64, 32, 16})
         if (rowlen % c == 0 && rowlen / c <= 256) {
@@ -570,7 +616,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       // two X' stages; the raw-row ring as deep as the rest of shared memory allows (<= 6)
       int rst = 0;
       for (int r = 6; r >= 2 && !rst; --r)
-        if (gemm_t_smem_bytes(32, d->R, 2, true, 1, raw, r, d->K) <= 226 * 1024) rst = r;
+        if (gemm_t_smem_bytes(32, d->R, 2, true, 1, raw, r, d->K, pl.wsplit ? 2 : 1) <= 226 * 1024) rst = r;
       if (ib && rst) {
         pl.trans = pl.t_build = pl.t_wres = true;
         pl.t_stages = 2;
@@ -587,10 +633,14 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
-  off = align256(off + (size_t)pl.Kpad * taps * pl.Cw);
+  off = align256(off + (size_t)pl.Kpad * taps * pl.Cw * bparts);
   if (pl.trans) {
     pl.pk_wt = off;
-    off = align256(off + (size_t)pl.t_Kt * taps * pl.Cw);
+    off = align256(off + (size_t)pl.t_Kt * taps * pl.Cw * bparts);
+  }
+  if (pl.any_zpw) {   // the per-channel zero points, for the packing and folding kernels
+    pl.pk_zpv = off;
+    off = align256(off + (size_t)d->K * 4);
   }
   pl.pk_off = off;
   off = align256(off + (size_t)pl.ct.ncr * pl.ct.ncc * pl.Kpad * 4);
@@ -611,7 +661,7 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     pl.ws_pad = w;
     w = align256(w + (size_t)d->N * d->H * pl.gW * pl.Ct);
   }
-  if (d->kernel_zero_point != 0) {
+  if (pl.any_zpw && !pl.wsplit) {
     pl.ws_pixsum = w;
     w = align256(w + (size_t)d->N * d->H * d->W * 4);
     pl.ws_rowsum = w;
@@ -622,10 +672,12 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   if (plan_trace)
     std::fprintf(stderr,
                  "[qnn plan] N%d C%d %dx%d K%d %dx%d s%d: BK%d BN%d num_m%d num_n%d chunks%d stages%d kps%d b_res%d "
-                 "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB)\n",
+                 "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB) trans%d t_build%d "
+                 "wsplit%d\n",
                  d->N, d->C, d->H, d->W, d->K, d->R, d->S, d->stride_h, pl.BK, pl.BN, pl.num_m, pl.num_n,
                  pl.nchunks, pl.stages, pl.kps, pl.b_res_kb, (int)pl.im2col, (int)pl.fold, (int)pl.pad_copy,
-                 (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes);
+                 (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes, (int)pl.trans,
+                 (int)pl.t_build, (int)pl.wsplit);
   return QNN_OK;
 }
 
@@ -654,9 +706,16 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
     }
   }
   cudaError_t e;
+  // per-channel weight zero points on the device (packing / folding kernels read them)
+  const int32_t* zpv_d = nullptr;
+  if ((pl.depthwise && pl.zp_vec) || (!pl.depthwise && pl.any_zpw)) {
+    e = cudaMemcpyAsync(pk + pl.pk_zpv, pl.zpv.data(), pl.zpv.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return QNN_ERR_CUDA;
+    zpv_d = reinterpret_cast<const int32_t*>(pk + pl.pk_zpv);
+  }
   if (pl.depthwise) {
     e = launch_pack_dw_weights(kernel, w_signed, d->kernel_zero_point, reinterpret_cast<int16_t*>(pk + pl.pk_w), d->C,
-                               d->R * d->S, s);
+                               d->R * d->S, s, zpv_d);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     if (bias)
       e = cudaMemcpyAsync(pk + pl.pk_bias, bias, (size_t)d->C * 4, cudaMemcpyDeviceToDevice, s);
@@ -677,18 +736,22 @@ static qnn_status_t conv_prepack(const qnn_conv2d_desc_t* d, const void* kernel,
       if (e != cudaSuccess) return QNN_ERR_CUDA;
     }
   } else {
-    // folded: each filter row r is one GEMM tap whose S*C channels are contiguous in OHWI
+    // folded: each filter row r is one GEMM tap whose S*C channels are contiguous in OHWI;
+    // wsplit: W - zp_W[k] in two s8 k-block sets (Term 3 in the contraction)
+    const int sp = pl.wsplit ? 1 : 0;
     if (pl.fold)
-      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R, d->S * d->C, pl.Cw, pl.Kpad, s);
+      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R, d->S * d->C, pl.Cw, pl.Kpad, s, 0, sp, w_signed, zpv_d);
     else
-      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s);
+      e = launch_pack_weights(kernel, pk + pl.pk_w, d->K, d->R * d->S, d->C, pl.Cw, pl.Kpad, s, 0, sp, w_signed, zpv_d);
     if (e == cudaSuccess && pl.trans)
-      e = pl.fold ? launch_pack_weights(kernel, pk + pl.pk_wt, d->K, d->R, d->S * d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1)
-                  : launch_pack_weights(kernel, pk + pl.pk_wt, d->K, 1, d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1);
+      e = pl.fold ? launch_pack_weights(kernel, pk + pl.pk_wt, d->K, d->R, d->S * d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1,
+                                        sp, w_signed, zpv_d)
+                  : launch_pack_weights(kernel, pk + pl.pk_wt, d->K, 1, d->C, pl.Cw, pl.t_Kt, s, /*perm32=*/1, sp,
+                                        w_signed, zpv_d);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = launch_fold_offsets(kernel, w_signed, bias, d->K, d->R, d->S, d->C, d->input_zero_point, d->kernel_zero_point,
                             pl.ct, reinterpret_cast<int32_t*>(pk + pl.pk_off),
-                            reinterpret_cast<int64_t*>(pk + pl.pk_off64), pl.Kpad, s);
+                            reinterpret_cast<int64_t*>(pk + pl.pk_off64), pl.Kpad, s, zpv_d);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
     e = cudaMemcpyAsync(pk + pl.pk_rowcls, pl.rowcls.data(), pl.rowcls.size(), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
@@ -764,7 +827,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     {
       int64_t wlo, whi;
       dtype_range(d->kernel_dtype, &wlo, &whi);
-      p.w_fits_s8 = wlo - d->kernel_zero_point >= -128 && whi - d->kernel_zero_point <= 127;
+      p.w_fits_s8 = true;
+      for (int32_t z : pl.zpv) p.w_fits_s8 = p.w_fits_s8 && wlo - z >= -128 && whi - z <= 127;
     }
     if (!force_tc && !force_generic && pl.requant) {
       int64_t qlo, qhi;
@@ -850,7 +914,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     a_pitch = pl.Ct;
   }
   const int32_t* rowsum = nullptr;
-  if (d->kernel_zero_point != 0) {
+  if (pl.any_zpw && !pl.wsplit) {
     int32_t* pixsum = reinterpret_cast<int32_t*>(wsb + pl.ws_pixsum);
     e = launch_pixel_sums(input, a_signed, pl.in_cs, d->C, (long long)d->N * d->H * d->W, pixsum, s);
     if (e != cudaSuccess) return QNN_ERR_CUDA;
@@ -893,7 +957,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         okx = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmTBN);
       }
       bool okt = okx &&
-                 encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)taps * pl.Cw, (uint64_t)pl.t_Kt, (uint64_t)taps * pl.Cw, pl.BK,
+                 encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), (uint64_t)pl.t_Kt,
+                           (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), pl.BK,
                            128) &&
                  encode_2d(&tmC, output, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)pl.out_cs, out_rb, kGemmTBN / 4) &&
                  (!res || encode_2d(&tmR, res->ptr, (uint64_t)d->K, (uint64_t)pl.M, (uint64_t)res_cs, out_rb,
@@ -931,7 +996,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
           tp.fdQ = make_fastdiv((uint32_t)pl.Q);
           tp.fdP = make_fastdiv((uint32_t)pl.P);
         }
-        tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights, B = activations
+        tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights (or split parts), B = activations
+        tp.wsplit = pl.wsplit;
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
         tp.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
         tp.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
@@ -992,7 +1058,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   else
     ok = encode_2d(&tmA, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmBM);
   if (!ok) return QNN_ERR_UNSUPPORTED;
-  ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)taps * pl.Cw, (uint64_t)pl.Kpad, (uint64_t)taps * pl.Cw, pl.BK,
+  ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), (uint64_t)pl.Kpad,
+                 (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), pl.BK,
                  pl.BN);
   if (!ok) return QNN_ERR_UNSUPPORTED;
   // 8-bit output through per-warp TMA stores when the output pitch allows it
@@ -1076,7 +1143,9 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.a_slot_bytes = pl.a_slot_bytes;
     p.a_raw_bytes = pl.a_raw_bytes;
   }
-  p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8, kGemmBM, pl.BN);
+  // (split weights are s8 parts whatever the kernel dtype)
+  p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8 || pl.wsplit, kGemmBM, pl.BN);
+  p.wsplit = pl.wsplit;
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
   ep.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);
@@ -1089,7 +1158,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   ep.ncls = pl.ct.ncr * pl.ct.ncc;
   ep.tma_store = tma_store;
   ep.rowsum = rowsum;
-  ep.zpW = d->kernel_zero_point;
+  ep.zpW = pl.wsplit ? 0 : d->kernel_zero_point;
   ep.out = output;
   ep.out_pitch = pl.out_cs;
   ep.Kpad = pl.Kpad;
@@ -1123,6 +1192,7 @@ static qnn_conv2d_desc_t dense_as_conv(const qnn_dense_desc_t* d) {
   c.in_cstride = d->lda; c.out_cstride = d->ldc;
   c.input_dtype = d->a_dtype; c.kernel_dtype = d->w_dtype;
   c.input_zero_point = d->zp_A; c.kernel_zero_point = d->zp_W;
+  c.kernel_zero_points = d->zp_Ws; c.num_kernel_zero_points = d->n_zpW;
   c.input_scale = d->s_A; c.kernel_scales = d->s_W; c.num_kernel_scales = d->n_sW;
   return c;
 }

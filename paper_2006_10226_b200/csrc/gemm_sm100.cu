@@ -70,16 +70,17 @@ constexpr bool kInstrument = false;
 // Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
 // commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes,
-                       int a_stage_bytes) {
-  const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK;
-  const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * b : stages * (a + b * kps);
+                       int a_stage_bytes, int bparts) {
+  // (bparts = 2: split weights, two B k-blocks per A k-block; b_res_kb then counts both parts)
+  const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK * bparts;
+  const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * (b / bparts) : stages * (a + b * kps);
   return 1024 + ring + (size_t)stages * raw_bytes + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
 }
 
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes) {
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes, int bparts) {
   const size_t budget = 227 * 1024;
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes) > budget) --s;
+  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes, bparts) > budget) --s;
   return s;
 }
 
@@ -103,12 +104,17 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // unless `acc`.
 template <int KS>
 __device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64_t bd, uint32_t idesc, int R, int S,
-                                             uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16, uint32_t acc) {
+                                             uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16, uint32_t acc,
+                                             uint32_t bsplit16) {
   for (int r = 0; r < R; ++r) {
     uint64_t ad = ad_row;
     for (int s = 0; s < S; ++s) {
 #pragma unroll
-      for (int k = 0; k < KS; ++k) umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, k ? 1u : acc);
+      for (int k = 0; k < KS; ++k) {
+        umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, k ? 1u : acc);
+        // split weights (zp_W folded): the second s8 part of W - zp_W against the same A
+        if (bsplit16) umma_i8(d, ad + 2 * k, bd + bsplit16 + 2 * k, idesc, 1u);
+      }
       acc = 1;
       ad += a_col16;
       bd += b_tap16;
@@ -119,13 +125,13 @@ __device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64
 
 __device__ __forceinline__ void issue_mma(int ksteps, uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, int R,
                                           int S, uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16,
-                                          uint32_t acc) {
+                                          uint32_t acc, uint32_t bsplit16) {
   if (ksteps == 4)
-    issue_mma_ks<4>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
+    issue_mma_ks<4>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
   else if (ksteps == 2)
-    issue_mma_ks<2>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
+    issue_mma_ks<2>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
   else if (ksteps == 1)
-    issue_mma_ks<1>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc);
+    issue_mma_ks<1>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
 }
 
 template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES>
@@ -145,11 +151,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nsets = gemm_epi_sets(BN, p.num_n_tiles, nepi);
   const uint32_t a_bytes = kGemmBM * BK, b_bytes = BN * BK;
   const bool b_res = p.b_res;
+  const int bparts = p.wsplit ? 2 : 1;   // split weights: two B k-blocks per A k-block
   const int kps = p.kps;                   // k-blocks per pipeline stage
   uint8_t* sA = smem;
   const size_t a_stage = p.a_stage_bytes ? (size_t)p.a_stage_bytes : (size_t)kps * a_bytes;   // A bytes / stage
   uint8_t* sB = smem + (size_t)stages * a_stage;   // ring of B stages, or the resident B (num_kb blocks)
-  uint8_t* sRaw = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes);   // a_build rows
+  uint8_t* sRaw = sB + (b_res ? (size_t)p.num_kb * b_bytes : (size_t)stages * kps * b_bytes) * bparts;   // a_build rows
   uint8_t* sOut = sRaw + (size_t)stages * p.a_raw_bytes;
   const bool tracing = kInstrument && p.trace != nullptr && blockIdx.x == 0;
   const int dbg = kInstrument ? p.dbg : 0;
@@ -225,9 +232,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (b_res && blockIdx.x < num_tiles) {
       // weights are shared by every tile of this CTA: load them once
       if (leader) {
-        mbar_arrive_expect_tx(bres_full, (uint32_t)p.num_kb * b_bytes);
-        // (a CTA keeps one N tile for all its tiles: grid % num_n == 0, see the host plan)
-        for (int kb = 0; kb < p.num_kb; ++kb)
+        mbar_arrive_expect_tx(bres_full, (uint32_t)(p.num_kb * bparts) * b_bytes);
+        // (a CTA keeps one N tile for all its tiles: grid % num_n == 0, see the host plan;
+        // split weights: part a's num_kb k-blocks, then part b's)
+        for (int kb = 0; kb < p.num_kb * bparts; ++kb)
           tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, n_first * BN);
       }
       __syncwarp();
@@ -327,10 +335,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
           if (tracing && it_p < 2048) trace_at(p.trace, it_p);
-          mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * ((b_res ? 0 : b_bytes) + (skip_a ? 0 : a_bytes)));
+          mbar_arrive_expect_tx(&full[stage],
+                                (uint32_t)nk * ((b_res ? 0 : b_bytes * bparts) + (skip_a ? 0 : a_bytes)));
           uint8_t* dA = sA + (size_t)stage * a_stage;
-          uint8_t* dB = sB + (size_t)(stage * kps) * b_bytes;
-          for (int t2 = 0; t2 < nk; ++t2, dA += a_bytes, dB += b_bytes) {
+          uint8_t* dB = sB + (size_t)(stage * kps) * b_bytes * bparts;
+          for (int t2 = 0; t2 < nk; ++t2, dA += a_bytes, dB += b_bytes * bparts) {
             const int kb = kb0 + t2;
             if (skip_a) {
             } else if (p.im2col) {
@@ -339,7 +348,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             } else {
               tma_load_2d(dA, &tmA, &full[stage], kb * BK, m0);
             }
-            if (!b_res) tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
+            if (!b_res) {
+              tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
+              if (bparts == 2) tma_load_2d(dB + b_bytes, &tmB, &full[stage], (p.num_kb + kb) * BK, n_blk * BN);
+            }
             if (++kc == p.nchunks) {
               kc = 0;
               if (++ks == p.S) {
@@ -465,6 +477,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int S_taps = a_rows ? p.S : 1, R_taps = a_rows ? num_kb / (p.S * nchunks) : 1;
     const uint32_t a_col16 = (uint32_t)BK >> 4, a_row16 = (uint32_t)(p.a_Wp * BK) >> 4;
     const uint32_t b_tap16 = (uint32_t)(nchunks * b_bytes) >> 4;
+    // split weights: part b sits num_kb k-blocks after part a when resident, right after it
+    // (interleaved per k-block) when streamed
+    const uint32_t bsplit16 = bparts == 2 ? (b_res ? ((uint32_t)num_kb * b_bytes) >> 4 : b_bytes >> 4) : 0u;
     // with two issuers, issuer mw takes the tiles i = mw (mod 2) and their sub-ring (producer)
     const int r_base = nmw == 2 ? mw * (stages >> 1) : 0, r_end = nmw == 2 ? r_base + (stages >> 1) : stages;
     stage = r_base;
@@ -491,7 +506,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
             const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage) + (uint32_t)(off0 * BK)) >> 4);
             const uint64_t bd = bdesc0 + (((uint32_t)kc * b_bytes) >> 4);
-            issue_mma(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0);
+            issue_mma(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0, bsplit16);
             umma_commit(&empty[stage]);
           }
           __syncwarp();
@@ -511,8 +526,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
           // descriptors advance by (byte offset >> 4) in the start-address field
           const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage)) >> 4);
-          const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb0 : stage * kps) * b_bytes) >> 4);
-          issue_mma(ksteps, d_tmem, ad, bd, idesc, 1, nk, 0, a_bytes >> 4, b_bytes >> 4, kb0 != 0);
+          const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb0 : stage * kps * bparts) * b_bytes) >> 4);
+          issue_mma(ksteps, d_tmem, ad, bd, idesc, 1, nk, 0, a_bytes >> 4, (b_bytes * (b_res ? 1 : bparts)) >> 4,
+                    kb0 != 0, bsplit16);
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -841,8 +857,9 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
     if (e != cudaSuccess) return e;
     if (dev < 64) attr_done[dev] = 1;
   }
-  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb : 0, p.kps,
-                                      p.a_raw_bytes, p.a_stage_bytes);
+  const int bparts = p.wsplit ? 2 : 1;
+  const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb * bparts : 0,
+                                      p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();

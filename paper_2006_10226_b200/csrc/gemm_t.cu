@@ -192,17 +192,19 @@ constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers a
 // carries its weight k-block next to the activation k-block.  build_raw_bytes >= 0: build mode,
 // a stage holds all num_kb X' k-blocks of a tile plus its raw input rows (weights resident)
 size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes,
-                         int rstages, int out_rb) {
+                         int rstages, int out_rb, int wparts) {
+  // (wparts = 2: split weights, two weight k-blocks per activation k-block)
   const size_t stage = build_raw_bytes >= 0 ? (size_t)num_kb * kTBN * BK
-                                            : (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK);
+                                            : (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK * wparts);
   const size_t raw = build_raw_bytes >= 0 ? (size_t)rstages * build_raw_bytes : 0;
-  return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK : 0) + raw +
+  return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK * wparts : 0) + raw +
          (size_t)4 * kTCols * out_rb * stage_bufs + 256;
 }
 
-int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes, int rstages, int out_rb) {
+int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes, int rstages, int out_rb,
+                      int wparts) {
   int s = 8;
-  while (s > 1 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs, build_raw_bytes, rstages, out_rb) >
+  while (s > 1 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs, build_raw_bytes, rstages, out_rb, wparts) >
                       (size_t)kTSmemMax)
     --s;
   return s;
@@ -219,11 +221,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
   const uint32_t x_bytes = (uint32_t)kTBN * BK, w_bytes = (uint32_t)kTBM * BK;
   const bool w_res = p.w_res;
   const bool build = p.build;
+  const int wparts = p.wsplit ? 2 : 1;   // split weights (zp_W folded): two weight k-blocks per k-block
   // X: stages x [256 pixels][BK] (build mode: stages x num_kb x [256 pixels][32], built in smem)
   const size_t x_stage = build ? (size_t)num_kb * x_bytes : (size_t)x_bytes;
   uint8_t* sX = smem;
   uint8_t* sW = sX + (size_t)stages * x_stage;         // num_kb (resident) or stages x [128 channels][BK]
-  uint8_t* sRaw = sW + (size_t)(w_res ? num_kb : stages) * w_bytes;   // build: stages x raw input rows
+  uint8_t* sRaw = sW + (size_t)(w_res ? num_kb : stages) * w_bytes * wparts;   // build: stages x raw input rows
   uint8_t* sOut = sRaw + (build ? (size_t)p.rstages * p.b_raw_bytes : 0);   // 4 groups x [kTCols px][out_rb]
   const uint32_t out_rb = (uint32_t)p.out_rb;   // staging row bytes: 128, or 64 / 32 when K_out is 64 / 32
   // epilogue warps: the quads holding live channels (all 4, or K_out / 32 in build mode, whose
@@ -267,8 +270,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
   if (warp == kProdWarp) {
     const bool leader = elect_one();
     if (leader && w_res && px_first < npt) {
-      mbar_arrive_expect_tx(&wfull, (uint32_t)num_kb * w_bytes);
-      for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
+      // (split weights: part a's num_kb k-blocks, then part b's)
+      mbar_arrive_expect_tx(&wfull, (uint32_t)(num_kb * wparts) * w_bytes);
+      for (int kb = 0; kb < num_kb * wparts; ++kb)
+        tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
     }
     int stage = 0;
     uint32_t phase = 0;
@@ -302,9 +307,14 @@ __global__ void __launch_bounds__(kTThreads, 1)
         QNN_T_WAIT(&empty[stage], phase ^ 1);
         if (leader && kb == 0) t_trace(p.trace, 0, (pt - px_first) / px_step);
         if (leader) {
-          mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes));
+          mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes * wparts));
           tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
-          if (!w_res) tma_load_2d(sW + (size_t)stage * w_bytes, &tmW, &full[stage], kb * BK, ch * kTBM);
+          if (!w_res) {
+            tma_load_2d(sW + (size_t)stage * w_bytes * wparts, &tmW, &full[stage], kb * BK, ch * kTBM);
+            if (wparts == 2)
+              tma_load_2d(sW + (size_t)stage * w_bytes * 2 + w_bytes, &tmW, &full[stage], (num_kb + kb) * BK,
+                          ch * kTBM);
+          }
         }
         __syncwarp();
         if (++stage == stages) {
@@ -334,7 +344,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
         if (leader) {
           t_trace(p.trace, 192, it);
           const uint64_t xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
-          for (int kb = 0; kb < num_kb; ++kb) umma_i8(d, wdesc0 + (uint64_t)kb * w16, xd + (uint64_t)kb * x16, idesc, kb != 0);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            umma_i8(d, wdesc0 + (uint64_t)kb * w16, xd + (uint64_t)kb * x16, idesc, kb != 0);
+            if (wparts == 2)   // split weights: part b, num_kb resident blocks on
+              umma_i8(d, wdesc0 + (uint64_t)(num_kb + kb) * w16, xd + (uint64_t)kb * x16, idesc, 1u);
+          }
           umma_commit(&empty[stage]);
           umma_commit(&tfull[acc]);
           t_trace(p.trace, 256, it);
@@ -351,9 +365,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
         tc_fence_after();
         if (leader && kb == 0) t_trace(p.trace, 192, it);
         if (leader) {
-          const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage) * w16, xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
+          const uint64_t wd = wdesc0 + (uint64_t)(w_res ? kb : stage * wparts) * w16,
+                         xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
+          // split weights: part b resident num_kb blocks on, or right after part a in the stage
+          const uint64_t wsplit16 = wparts == 2 ? (uint64_t)(w_res ? num_kb : 1) * w16 : 0;
           if (!(kTInstrument && (p.dbg & 8)))   // (instrumented builds: 8 skips the MMAs)
-            for (int k = 0; k < ksteps; ++k) umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < ksteps; ++k) {
+              umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+              if (wparts == 2) umma_i8(d, wd + wsplit16 + 2 * k, xd + 2 * k, idesc, 1u);
+            }
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -590,7 +610,7 @@ cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
                           cudaStream_t stream) {
   const bool res = p.has_res;
   const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res, p.stage_bufs,
-                                       p.build ? p.b_raw_bytes : -1, p.rstages, p.out_rb);
+                                       p.build ? p.b_raw_bytes : -1, p.rstages, p.out_rb, p.wsplit ? 2 : 1);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);

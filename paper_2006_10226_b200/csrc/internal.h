@@ -80,6 +80,7 @@ struct GemmTParams {
   const int64_t* off64;  // [Kpad] (single border class)
   int32_t zp_out, lo, hi;
   int stage_bufs;         // output staging buffers per column group (1 or 2)
+  int wsplit;             // weights packed as W - zp_W[k] in two s8 parts: two A k-blocks per k-block
   int out_rb;             // staging / TMA-store row bytes: 128 (min(K_out, 128) in build mode)
   // build mode (small-C stems, K_out <= 64): the B operand X'[pixel][s*C + c] (one 32-byte
   // k-block per filter row, width fold of P:259's zero-point-padded input) is built in shared
@@ -94,9 +95,9 @@ struct GemmTParams {
   unsigned long long* trace;   // QNN_GEMM_TRACE (instrumented builds only): CTA 0 clock64 events
 };
 size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes = -1,
-                         int rstages = 0, int out_rb = 128);
+                         int rstages = 0, int out_rb = 128, int wparts = 1);
 int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes = -1, int rstages = 0,
-                      int out_rb = 128);
+                      int out_rb = 128, int wparts = 1);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream);
@@ -140,6 +141,7 @@ struct GemmParams {
   FastDiv fdT, fdWp;
   GemmEpilogue e;
   int mma2;   // two MMA-issuing warps taking alternate tiles (narrow tiles)
+  int wsplit; // weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction)
 };
 
 constexpr int kGemmBM = 128;
@@ -169,8 +171,9 @@ __host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles, int nepi =
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0,
-                       int a_stage_bytes = 0);
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0, int a_stage_bytes = 0);
+                       int a_stage_bytes = 0, int bparts = 1);
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0, int a_stage_bytes = 0,
+                    int bparts = 1);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
@@ -184,12 +187,13 @@ struct ClassTable {
 };
 
 cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad,
-                                cudaStream_t s, int perm32 = 0);
+                                cudaStream_t s, int perm32 = 0, int split = 0, int w_signed = 1,
+                                const int32_t* zpv = nullptr);
 cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
                                 int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int64_t* off64, int Kpad,
-                                cudaStream_t s);
+                                cudaStream_t s, const int32_t* zpv = nullptr);
 cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int16_t* Wd, int C, int RS,
-                                   cudaStream_t s);
+                                   cudaStream_t s, const int32_t* zpv = nullptr);
 cudaError_t launch_pad_channels(const void* in, long long in_cstride, void* out, int Cp, long long npix, int C,
                                 cudaStream_t s);
 cudaError_t launch_fold_width(const void* in, long long in_cstride, void* out, int N, int H, int W, int C, int Q, int S,

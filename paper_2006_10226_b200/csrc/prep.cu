@@ -21,36 +21,52 @@ namespace qnn {
 
 // perm32: row r of every 32-row group holds channel 4*(r % 8) + (r / 8) % 4 of that group -- the
 // TMEM lane order of the channel-major GEMM (gemm_t.cu), whose 16x256b TMEM loads then hand a
-// thread four consecutive output channels of one pixel
+// thread four consecutive output channels of one pixel.
+// split (weight zero points, Term 3 folded into the contraction): row k holds W - zp_W[k] as two
+// s8 k-block sets, [RS*Cw part a][RS*Cw part b] with a = clamp(W', -128, 127), b = W' - a, so
+// sum_c A * (a + b) = sum_c A * (W - zp_W[k]) exactly (W' in [-256, 254], checked on the host)
 __global__ void pack_weights_kernel(const uint8_t* __restrict__ W, uint8_t* __restrict__ Wp, int K, int RS, int C,
-                                    int Cw, int Kpad, int perm32) {
-  const long long total = (long long)Kpad * RS * Cw;
+                                    int Cw, int Kpad, int perm32, int split, int w_signed,
+                                    const int32_t* __restrict__ zpv) {
+  const int row_w = (split ? 2 : 1) * RS * Cw;
+  const long long total = (long long)Kpad * row_w;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(i % Cw);
-    const long long t = i / Cw;
-    const int tap = (int)(t % RS);
-    const int row = (int)(t / RS);
+    const int col = (int)(i % row_w);
+    const int row = (int)(i / row_w);
+    const int part = col / (RS * Cw), cc = col - part * RS * Cw;
+    const int c = cc % Cw, tap = cc / Cw;
     const int k = perm32 ? (row & ~31) | (4 * (row & 7) + ((row >> 3) & 3)) : row;
     uint8_t v = 0;
-    if (k < K && c < C) v = W[((long long)k * RS + tap) * C + c];
+    if (k < K && c < C) {
+      const uint8_t b = W[((long long)k * RS + tap) * C + c];
+      if (split) {
+        const int wv = (w_signed ? (int)(int8_t)b : (int)b) - zpv[k];
+        const int a = min(max(wv, -128), 127);
+        v = (uint8_t)(int8_t)(part == 0 ? a : wv - a);
+      } else {
+        v = b;
+      }
+    }
     Wp[i] = v;
   }
 }
 
 cudaError_t launch_pack_weights(const void* W, void* Wp, int K, int RS, int C, int Cw, int Kpad, cudaStream_t s,
-                                int perm32) {
-  const long long total = (long long)Kpad * RS * Cw;
+                                int perm32, int split, int w_signed, const int32_t* zpv) {
+  const long long total = (long long)Kpad * RS * Cw * (split ? 2 : 1);
   const int threads = 256;
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 4096);
-  pack_weights_kernel<<<blocks, threads, 0, s>>>((const uint8_t*)W, (uint8_t*)Wp, K, RS, C, Cw, Kpad, perm32);
+  pack_weights_kernel<<<blocks, threads, 0, s>>>((const uint8_t*)W, (uint8_t*)Wp, K, RS, C, Cw, Kpad, perm32, split,
+                                                 w_signed, zpv);
   count_launch();
   return cudaGetLastError();
 }
 
 __global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed, const int32_t* __restrict__ bias,
-                                    int K, int R, int S, int C, int32_t zpA, int32_t zpW, ClassTable ct,
-                                    int32_t* __restrict__ off, int64_t* __restrict__ off64, int Kpad) {
+                                    int K, int R, int S, int C, int32_t zpA, int32_t zpW_scalar, ClassTable ct,
+                                    int32_t* __restrict__ off, int64_t* __restrict__ off64, int Kpad,
+                                    const int32_t* __restrict__ zpv) {
   const int ncls = ct.ncr * ct.ncc;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= ncls * Kpad) return;
@@ -62,6 +78,7 @@ __global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed,
   }
   const int rc = cls / ct.ncc, cc = cls - rc * ct.ncc;
   const int r0 = ct.r_lo[rc], r1 = ct.r_hi[rc], s0 = ct.s_lo[cc], s1 = ct.s_hi[cc];
+  const long long zpW = zpv ? zpv[k] : zpW_scalar;   // per-channel weight zero point (f4)
   long long colsum = 0;
   int nvalid = 0;
   for (int r = r0; r <= r1; ++r)
@@ -79,28 +96,28 @@ __global__ void fold_offsets_kernel(const uint8_t* __restrict__ W, int w_signed,
 
 cudaError_t launch_fold_offsets(const void* W, int w_signed, const int32_t* bias, int K, int R, int S, int C,
                                 int32_t zpA, int32_t zpW, const ClassTable& ct, int32_t* off, int64_t* off64,
-                                int Kpad, cudaStream_t s) {
+                                int Kpad, cudaStream_t s, const int32_t* zpv) {
   const int total = ct.ncr * ct.ncc * Kpad;
   fold_offsets_kernel<<<(total + 127) / 128, 128, 0, s>>>((const uint8_t*)W, w_signed, bias, K, R, S, C, zpA, zpW,
-                                                         ct, off, off64, Kpad);
+                                                         ct, off, off64, Kpad, zpv);
   count_launch();
   return cudaGetLastError();
 }
 
 // depthwise weights K x R x S x 1 (K == C) -> [R*S][C] int16 holding W - zp_W
 __global__ void pack_dw_weights_kernel(const uint8_t* __restrict__ W, int w_signed, int32_t zpW,
-                                       int16_t* __restrict__ Wd, int C, int RS) {
+                                       int16_t* __restrict__ Wd, int C, int RS, const int32_t* __restrict__ zpv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C * RS) return;
   const int tap = i / C, c = i - tap * C;
   const uint8_t b = W[(long long)c * RS + tap];
   const int v = w_signed ? (int)(int8_t)b : (int)b;
-  Wd[i] = (int16_t)(v - zpW);
+  Wd[i] = (int16_t)(v - (zpv ? zpv[c] : zpW));
 }
 
 cudaError_t launch_pack_dw_weights(const void* W, int w_signed, int32_t zpW, int16_t* Wd, int C, int RS,
-                                   cudaStream_t s) {
-  pack_dw_weights_kernel<<<(C * RS + 255) / 256, 256, 0, s>>>((const uint8_t*)W, w_signed, zpW, Wd, C, RS);
+                                   cudaStream_t s, const int32_t* zpv) {
+  pack_dw_weights_kernel<<<(C * RS + 255) / 256, 256, 0, s>>>((const uint8_t*)W, w_signed, zpW, Wd, C, RS, zpv);
   count_launch();
   return cudaGetLastError();
 }

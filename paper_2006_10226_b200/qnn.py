@@ -59,14 +59,16 @@ class Conv2dDesc(ctypes.Structure):
         ("input_dtype", ctypes.c_int), ("kernel_dtype", ctypes.c_int),
         ("input_zero_point", ctypes.c_int32), ("kernel_zero_point", ctypes.c_int32),
         ("input_scale", ctypes.c_float), ("kernel_scales", ctypes.POINTER(ctypes.c_float)),
-        ("num_kernel_scales", ctypes.c_int32)]
+        ("num_kernel_scales", ctypes.c_int32), ("kernel_zero_points", ctypes.POINTER(ctypes.c_int32)),
+        ("num_kernel_zero_points", ctypes.c_int32)]
 
 
 class DenseDesc(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("lda", ctypes.c_int32),
                 ("ldc", ctypes.c_int32), ("a_dtype", ctypes.c_int), ("w_dtype", ctypes.c_int),
                 ("zp_A", ctypes.c_int32), ("zp_W", ctypes.c_int32), ("s_A", ctypes.c_float),
-                ("s_W", ctypes.POINTER(ctypes.c_float)), ("n_sW", ctypes.c_int32)]
+                ("s_W", ctypes.POINTER(ctypes.c_float)), ("n_sW", ctypes.c_int32),
+                ("zp_Ws", ctypes.POINTER(ctypes.c_int32)), ("n_zpW", ctypes.c_int32)]
 
 
 def lib() -> ctypes.CDLL:
@@ -193,7 +195,13 @@ class PackedConv2d:
         d.input_dtype = _dtcode(input_dtype)
         d.kernel_dtype = _dtcode(w.dtype)
         d.input_zero_point = int(zp_A)
-        d.kernel_zero_point = int(zp_W)
+        if isinstance(zp_W, (int,)) or (hasattr(zp_W, "ndim") and getattr(zp_W, "ndim") == 0):
+            d.kernel_zero_point = int(zp_W)
+        else:   # per-channel weight zero points (f4)
+            self._zps = _ints(zp_W)
+            d.kernel_zero_point = 0
+            d.kernel_zero_points = ctypes.cast(self._zps, ctypes.POINTER(ctypes.c_int32))
+            d.num_kernel_zero_points = len(self._zps)
         d.input_scale = float(s_A)
         d.kernel_scales = ctypes.cast(self._scales, ctypes.POINTER(ctypes.c_float))
         d.num_kernel_scales = len(self._scales)
@@ -274,7 +282,13 @@ class PackedDense:
         d.M, d.N, d.K, d.lda, d.ldc = int(M), int(N), int(K), 0, 0
         d.a_dtype = _dtcode(a_dtype)
         d.w_dtype = _dtcode(w.dtype)
-        d.zp_A, d.zp_W, d.s_A = int(zp_A), int(zp_W), float(s_A)
+        if isinstance(zp_W, (int,)) or (hasattr(zp_W, "ndim") and getattr(zp_W, "ndim") == 0):
+            d.zp_A, d.zp_W, d.s_A = int(zp_A), int(zp_W), float(s_A)
+        else:   # per-channel weight zero points (f4)
+            self._zps = _ints(zp_W)
+            d.zp_A, d.zp_W, d.s_A = int(zp_A), 0, float(s_A)
+            d.zp_Ws = ctypes.cast(self._zps, ctypes.POINTER(ctypes.c_int32))
+            d.n_zpW = len(self._zps)
         d.s_W = ctypes.cast(self._scales, ctypes.POINTER(ctypes.c_float))
         d.n_sW = len(self._scales)
         self.desc = d

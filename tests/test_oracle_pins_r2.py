@@ -117,3 +117,31 @@ def test_dequantize_int32_vs_exact(orc):
             assert abs(Fraction(xi) - v) <= ulp, (qi, zp, float(s))
             if abs(qi - zp) <= 2**24:           # q - zp exact in fp32: a single rounding
                 assert xi == float(np.float32(float(v))) or abs(Fraction(xi) - v) <= ulp / 2
+
+
+@pytest.mark.parametrize("groups", [1, 6])
+def test_per_channel_weight_zero_points_vs_float64_library(orc, groups):
+    """f4 (per-channel zp_W): the oracle's channel-by-channel evaluation against torch's float64
+    conv of the zero-point-subtracted operands (exact below 2^53), with W - zp_W[k] broadcast."""
+    import torch
+    import torch.nn.functional as F
+    g = np.random.default_rng(31 + groups)
+    for trial in range(6):
+        C = 6
+        K = 6 if groups > 1 else int(g.integers(2, 9))
+        A = g.integers(0, 256, size=(2, C, 7, 8)).astype(np.uint8)
+        Wt = g.integers(-128, 128, size=(K, C // groups, 3, 3)).astype(np.int8)
+        zpA = int(g.integers(0, 256))
+        zpv = g.integers(-127, 128, size=K).astype(np.int32)
+        bias = g.integers(-999, 1000, size=K).astype(np.int32)
+        got = orc.conv2d_acc(A, Wt, zpA, zpv, bias, (1, 2), (1, 1, 0, 2), (1, 1), groups)
+        a = F.pad(torch.from_numpy(A.astype(np.float64) - zpA), (1, 2, 1, 0))
+        w = torch.from_numpy(Wt.astype(np.float64) - zpv.astype(np.float64)[:, None, None, None])
+        want = F.conv2d(a, w, stride=(1, 2), groups=groups).numpy().astype(np.int64) + bias[None, :, None, None]
+        assert np.array_equal(got, want), trial
+    Ad = g.integers(0, 256, size=(5, 40)).astype(np.uint8)
+    Wd = g.integers(0, 256, size=(7, 40)).astype(np.uint8)
+    zd = g.integers(0, 256, size=7)
+    got = orc.dense_acc(Ad, Wd, 17, zd)
+    want = (Ad.astype(np.int64) - 17) @ (Wd.astype(np.int64) - zd[:, None]).T
+    assert np.array_equal(got, want)
