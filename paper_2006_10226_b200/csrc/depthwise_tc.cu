@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kDwThreads, 1)
   uint64_t* tempty = tfull + kDwNacc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kDwNacc);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   constexpr int kProdWarp = kDwEpiWarps, kMmaWarp = kDwEpiWarps + 1;
   const int item_lo = (int)((long long)blockIdx.x * p.items / gridDim.x);
   const int item_hi = (int)((long long)(blockIdx.x + 1) * p.items / gridDim.x);

@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[8], rawfull[8],
       rawempty[8];
   __shared__ uint32_t tmem_slot;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches keep their loop state
+  // and UMMA / TMA operands in uniform registers (no R2UR per instruction)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   constexpr int kProdWarp = kTEpiWarps, kMmaWarp = kTEpiWarps + 1;
   const int nct = p.num_ch_tiles, npt = p.num_px_tiles;
   const int ch = blockIdx.x % nct;                  // fixed channel block (gridDim.x % nct == 0)

@@ -176,6 +176,8 @@ int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_byt
                     int bparts = 1);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
+cudaError_t launch_gemm_split(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
+                              const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // Prepack / auxiliary kernels (prep.cu)
