@@ -1112,14 +1112,6 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.trace = tr_env ? reinterpret_cast<unsigned long long*>(std::strtoull(tr_env, nullptr, 0)) : nullptr;
   }
   p.P = pl.P; p.Q = pl.Q; p.sh = d->stride_h; p.sw = pl.g_sw; p.pt = d->pad_t; p.pl = pl.g_pl;
-  {
-    // a second MMA issuer for narrow tiles, opt-in (QNN_MMA2=1): the two issuers take
-    // alternate tiles, each with its own half of the stage ring.  Measured on ResNet-50 b256:
-    // no gain on the layer1 3x3 convs (N=64, issue ~90 cycles/MMA is not their bound), 15-23%
-    // slower on the layer2 3x3 convs (half the pipeline depth per issuer).
-    static const bool mma2 = std::getenv("QNN_MMA2") != nullptr;
-    p.mma2 = mma2 && !pl.a_build && pl.BN <= 128 && gemm_acc_bufs(pl.BN) >= 2 && pl.stages >= 4;
-  }
   p.fdQ = make_fastdiv((uint32_t)pl.Q);
   p.fdPQ = make_fastdiv((uint32_t)(pl.P * pl.Q));
   if (pl.a_rows) {

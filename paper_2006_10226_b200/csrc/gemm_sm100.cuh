@@ -231,34 +231,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     const bool skip_a = dbg & 4;
     int m_blk = m_first, n_blk = n_first;
-    // two MMA issuers (p.mma2): CTA tile i is staged in sub-ring (i & 1) = [base, base + half),
-    // so each issuer waits on barriers only it consumes (exact parity waits)
-    const int half = stages >> 1;
-    int ring_stage[2] = {0, half};
-    uint32_t ring_phase[2] = {0, 0};
-    int r_base = 0, r_end = stages;
-    auto ring_enter = [&](int i) {
-      if (p.mma2) {
-        r_base = (i & 1) * half;
-        r_end = r_base + half;
-        stage = ring_stage[i & 1];
-        phase = ring_phase[i & 1];
-      }
-    };
-    auto ring_leave = [&](int i) {
-      if (p.mma2) {
-        ring_stage[i & 1] = stage;
-        ring_phase[i & 1] = phase;
-      }
-    };
-    int tile_i = 0;
     if (p.a_rows) {
       // one box per (tile, channel chunk): input rows p_first - pt .. + a_nri, columns -pl .. + Wp
       const uint32_t bytes = (uint32_t)(p.a_nri * p.a_Wp * BK);
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tile_i) {
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int n = (int)fdiv((uint32_t)m_blk, p.fdT), tt = m_blk - n * p.a_T;
         const int p_first = (int)fdiv((uint32_t)(tt * kGemmBM), p.fdWp);
-        ring_enter(tile_i);
         for (int kc = 0; kc < p.nchunks; ++kc) {
           if (tracing && leader && it_p < 256) trace_at(p.trace, 6300 + it_p);
           mbar_wait(&empty[stage], phase ^ 1);
@@ -270,12 +248,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           __syncwarp();
           ++it_p;
-          if (++stage == r_end) {
-            stage = r_base;
+          if (++stage == stages) {
+            stage = 0;
             phase ^= 1;
           }
         }
-        ring_leave(tile_i);
         QNN_NEXT_TILE();
       }
     }
@@ -315,7 +292,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       // (filter row, filter col, channel chunk) of the next k-block, advanced by counters
       int kr = 0, ks = 0, kc = 0;
-      ring_enter(tile_i);
       for (int kb0 = 0; kb0 < p.num_kb; kb0 += kps) {
         const int nk = min(kps, p.num_kb - kb0);
         if (tracing && leader && it_p < 256) trace_at(p.trace, 6300 + it_p);
@@ -351,13 +327,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
         ++it_p;
-        if (++stage == r_end) {
-          stage = r_base;
+        if (++stage == stages) {
+          stage = 0;
           phase ^= 1;
         }
       }
-      ring_leave(tile_i);
-      ++tile_i;
       QNN_NEXT_TILE();
     }
   } else if (p.a_build && warp >= nepi && warp < kEpiW) {
@@ -443,14 +417,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       QNN_NEXT_TILE();
     }
-  } else if (warp == kMmaWarp || (p.mma2 && warp == kMmaWarp - 2)) {
-    // ------------------------------------------------------------ MMA issuer(s)
-    // Warp-uniform loop; the elected lane issues every tcgen05.mma and its commits.  With
-    // p.mma2 (narrow tiles, where one issuing thread cannot keep the tensor pipe busy: ~68+
-    // cycles per MMA against 32-64 of tensor work at N <= 128) a second warp takes the odd
-    // tiles: each walks the shared stage ring in order and skips the other's stages.
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    // Warp-uniform loop; the elected lane issues every tcgen05.mma and its commits.
     const bool leader = elect_one();
-    const int mw = warp == kMmaWarp ? 0 : 1, nmw = p.mma2 ? 2 : 1;
     int stage = 0, it_m = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -467,12 +437,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // split weights: part b sits num_kb k-blocks after part a when resident, right after it
     // (interleaved per k-block) when streamed
     const uint32_t bsplit16 = SPLIT ? (b_res ? ((uint32_t)num_kb * b_bytes) >> 4 : b_bytes >> 4) : 0u;
-    // with two issuers, issuer mw takes the tiles i = mw (mod 2) and their sub-ring (producer)
-    const int r_base = nmw == 2 ? mw * (stages >> 1) : 0, r_end = nmw == 2 ? r_base + (stages >> 1) : stages;
-    stage = r_base;
     if (b_res) mbar_wait(bres_full, 0);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      if (nmw == 2 && (it & 1) != mw) continue;   // the other issuer's tile
       const int acc = it & (nacc - 1);
       const uint32_t acc_phase = (it >> acc_log) & 1;
       if (tracing && leader && it < 100) trace_at(p.trace, 7200 + it);
@@ -498,8 +464,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           __syncwarp();
           ++it_m;
-          if (++stage == r_end) {
-            stage = r_base;
+          if (++stage == stages) {
+            stage = 0;
             phase ^= 1;
           }
         }
@@ -520,8 +486,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
         ++it_m;
-        if (++stage == r_end) {
-          stage = r_base;
+        if (++stage == stages) {
+          stage = 0;
           phase ^= 1;
         }
       }

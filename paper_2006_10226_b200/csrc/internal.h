@@ -140,7 +140,6 @@ struct GemmParams {
   int a_stage_bytes;       // A bytes per pipeline stage (a_rows: a_nri * a_Wp * BK rounded up)
   FastDiv fdT, fdWp;
   GemmEpilogue e;
-  int mma2;   // two MMA-issuing warps taking alternate tiles (narrow tiles)
   int wsplit; // weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction)
 };
 
