@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage) + (uint32_t)(off0 * BK)) >> 4);
             const uint64_t bd = bdesc0 + (((uint32_t)kc * b_bytes) >> 4);
             issue_mma<SPLIT>(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0, bsplit16);
+            if (tracing && it_m < 64) trace_at(p.trace, 6100 + it_m);   // all MMAs of the stage issued
             umma_commit(&empty[stage]);
           }
           __syncwarp();

@@ -1,6 +1,8 @@
 // mma_rate2.cu — cycles per tcgen05.mma.kind::i8 (M=128, cta_group::1) vs swizzle mode of the K-major
 // operands (32/64/128-B rows), operand contents (zeros vs random bytes) and N.  Each MMA reads a
-// different 128-row A slice (walking a 64 KB ring, like the GEMM's pipeline stages).
+// different 128-row A slice (walking a 64 KB ring, like the GEMM's pipeline stages).  shift = 1 starts
+// each slice at a row offset that is not a multiple of the 8-row swizzle atom (the staged-row
+// 3x3 path addresses filter taps that way).
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/mma_rate2 tools/micro/mma_rate2.cu
 #include <cstdint>
@@ -21,7 +23,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, int rb) {
   return d;
 }
 
-__global__ void __launch_bounds__(128, 1) mma_rate(int N, int rb, int iters, int fill, long long* out) {
+__global__ void __launch_bounds__(128, 1) mma_rate(int N, int rb, int iters, int fill, int shift, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bar;
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int N, int rb, int iters, int
   const uint32_t tmem = tmem_slot;
   const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   // A slices: 128 rows x rb bytes each; K=32 per MMA -> rb/32 MMAs per slice
-  const int slice = 128 * rb, nslices = 65536 / slice, kst = rb / 32;
+  const int slice = 128 * rb, nslices = 65536 / slice / 2, kst = rb / 32;   // (half the ring: room for shifts)
   const int lk = __ffs(kst) - 1, smask = nslices - 1, kmask = kst - 1, lsl = __ffs(slice >> 4) - 1;
   if (threadIdx.x == 0) {
     const uint64_t a0 = sdesc(smem_u32(sa), rb), b0 = sdesc(smem_u32(sb), rb);
@@ -57,7 +59,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int N, int rb, int iters, int
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int m = i + j, sl = (m >> lk) & smask, k = m & kmask;
-        ad[j] = a0 + ((uint32_t)sl << lsl) + 2 * k;
+        const uint32_t rsh = shift ? (uint32_t)((m >> lk) * 5 % 61) * rb : 0u;   // row shift, bytes
+        ad[j] = a0 + ((uint32_t)sl << lsl) + (rsh >> 4) + 2 * k;
         bd[j] = b0 + 2 * k;
       }
       asm volatile(
@@ -86,12 +89,13 @@ int main() {
   cudaMalloc(&d_out, sizeof(long long));
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int iters = 8192;
-  printf("%4s %4s %5s %12s %12s\n", "N", "rowB", "fill", "cycles/MMA", "ideal(N/2)");
-  for (int fill : {0, 1})
+  printf("%4s %4s %5s %5s %12s %12s\n", "N", "rowB", "fill", "shift", "cycles/MMA", "ideal(N/2)");
+  for (int shift : {0, 1})
+  for (int fill : {1})
     for (int rb : {32, 64, 128})
       for (int N : {32, 64, 128, 256}) {
-        mma_rate<<<148, 128, 100 * 1024>>>(N, rb, iters, fill, d_out);
-        mma_rate<<<148, 128, 100 * 1024>>>(N, rb, iters, fill, d_out);
+        mma_rate<<<148, 128, 100 * 1024>>>(N, rb, iters, fill, shift, d_out);
+        mma_rate<<<148, 128, 100 * 1024>>>(N, rb, iters, fill, shift, d_out);
         long long cyc = 0;
         cudaMemcpy(&cyc, d_out, sizeof(cyc), cudaMemcpyDeviceToHost);
         cudaError_t e = cudaGetLastError();
@@ -99,7 +103,7 @@ int main() {
           printf("error %s\n", cudaGetErrorString(e));
           return 1;
         }
-        printf("%4d %4d %5d %12.1f %12d\n", N, rb, fill, (double)cyc / iters, N / 2);
+        printf("%4d %4d %5d %5d %12.1f %12d\n", N, rb, fill, shift, (double)cyc / iters, N / 2);
       }
   return 0;
 }

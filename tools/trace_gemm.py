@@ -55,3 +55,8 @@ wk = t[9200:9200 + 1600].reshape(100, 16); en = t[10900:10900 + 1600].reshape(10
 for i in (4, 5, 6):
     print("tile", i, "wake:", [int(x - t0) if x > 0 else None for x in wk[i]])
     print("       end :", [int(x - t0) if x > 0 else None for x in en[i]])
+# a_rows: MMA issue time per stage (stage start -> all its MMAs issued)
+st, iss = t[2048:2048 + 64], t[6100:6164]
+m = (st > 0) & (iss > 0)
+if m.sum():
+    print("a_rows MMA issue cycles per stage:", (iss[m] - st[m])[:20].tolist())
