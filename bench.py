@@ -152,18 +152,17 @@ class GpuResNet50:
     def replay(self):
         self.graph.replay()
 
-    def capture_alt(self):
-        """A second graph of the same step reading its image from a second device buffer, so
-        the e2e loop can copy step k+1's image in while step k computes (double buffering)."""
-        torch = self.torch
-        main_graph, main_img = self.graph, self.image_d
-        self.image_d_alt = torch.empty_like(main_img)
-        self.image_d = self.image_d_alt
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.step()
+    def capture_e2e(self, host_out):
+        """The step minus its quantize, with the logits dequantized straight into the pinned host
+        buffer `host_out` (qnn_dequantize_host): the graph an end-to-end step replays after
+        qnn_quantize_host has brought its image in."""
+        torch, q = self.torch, self.qnn
+        self.graph_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph_e2e):
+            self.stack.run()
+            self.fc(self.fc_in, out=self.fc_out)
+            q.qnn_dequantize_host(self.fc_out, host_out, self.logit_scale, [0], axis=-1)
         torch.cuda.synchronize()
-        self.graph_alt, self.graph, self.image_d = self.graph, main_graph, main_img
 
 
 # ----------------------------------------------------------------------------- full network (f1)
@@ -818,43 +817,42 @@ def main():
     ms_per_step = ms / args.steps
     value = G * args.steps / (ms / 1000.0)
 
-    # ---------------- e2e: host f32 image in (pinned H2D) -> graph -> logits out (D2H), same metric
+    # ---------------- e2e: host f32 image in -> logits out on the host, same metric, through the
+    # C-ABI host-buffer entry points: every step, qnn_quantize_host copies the step's f32 images
+    # from pinned host memory (copy engine, copy stream) into a device staging buffer and
+    # quantizes them on the compute stream; the graph (53 conv + fc) ends in qnn_dequantize_host,
+    # which writes the f32 logits straight into pinned host memory.  Two staging buffers: step
+    # k+1's copy overlaps step k's graph.  The timed region starts before the first copy and ends
+    # after the last logits reached the host.
+    from paper_2006_10226_b200 import qnn_quantize_host
     host_in = torch.from_numpy(model["image"]).pin_memory()
     host_out = torch.empty(net.logits.shape, dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 50))
-    # every step: its image H2D from pinned memory (copy stream, into the buffer the step's graph
-    # reads; double-buffered so step k+1's copy overlaps step k's compute), the graph, and the
-    # logits D2H; the timed region starts before the first copy and ends after the last D2H
-    net.capture_alt()
-    bufs, graphs = (net.image_d, net.image_d_alt), (net.graph, net.graph_alt)
+    net.capture_e2e(host_out)
+    staging = (torch.empty_like(net.image_d), torch.empty_like(net.image_d))
     cstream, copy_s = torch.cuda.current_stream(), torch.cuda.Stream()
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
     consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    img_scale, img_zp = [model["img_scale"]], [model["img_zp"]]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(cstream)
     copy_s.wait_event(e0)
-    with torch.cuda.stream(copy_s):
-        bufs[0].copy_(host_in, non_blocking=True)
-        copied[0].record(copy_s)
     for k in range(e2e_steps):
         b = k & 1
-        if k + 1 < e2e_steps:
-            with torch.cuda.stream(copy_s):
-                if k >= 1:
-                    copy_s.wait_event(consumed[1 - b])   # step k-1's graph is done with that buffer
-                bufs[1 - b].copy_(host_in, non_blocking=True)
-                copied[1 - b].record(copy_s)
-        cstream.wait_event(copied[b])
-        graphs[b].replay()
+        if k >= 2:
+            copy_s.wait_event(consumed[b])   # step k-2's quantize is done with this staging buffer
+        qnn_quantize_host(host_in, staging[b], net.q_image, img_scale, img_zp, "u8", copy_stream=copy_s,
+                          stream=cstream)
         consumed[b].record(cstream)
-        host_out.copy_(net.logits, non_blocking=True)
+        net.graph_e2e.replay()
     e1.record(cstream)
     torch.cuda.synchronize()
     ems = max_over_ranks(e0.elapsed_time(e1), dist if world > 1 else None, dev)
     e2e_value = G * e2e_steps / (ems / 1000.0)
+    # the last step's logits, read from the host buffer, equal the device-timed graph's
+    e2e_ok = bool(torch.equal(host_out, net.logits.cpu()))
     h2d = host_in.numel() * 4
     d2h = host_out.numel() * 4
 
@@ -1009,8 +1007,10 @@ def main():
         "conv_tops": round(conv_tops, 1), "conv_pct_int8_peak": round(100 * conv_tops / int8_peak, 2),
         "e2e": {"value": round(e2e_value, 1), "unit": "images/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "note": "pinned f32 images H2D (copy stream, double-buffered: step k+1's copy overlaps step k) "
-                        "+ graph + f32 logits D2H, every step"},
+                "api": "C-ABI qnn_quantize_host (pinned f32 in, copy engine) + graph + qnn_dequantize_host (f32 logits "
+                       "written into pinned host memory)", "logits_match_device_step": e2e_ok,
+                "note": "every step: pinned f32 images H2D (copy engine, double-buffered: step k+1's copy "
+                        "overlaps step k) + quantize + graph + f32 logits to pinned host memory"},
         "gpu_launches": int(net.launches_per_step * args.steps),
         "roofline": {"kernel": "tcgen05 GEMMs: qnn_gemm_i8_kernel + qnn_gemm_t_kernel (all 54 conv/fc launches "
                                "of a step)", "bound": "tensor",

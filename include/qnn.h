@@ -245,6 +245,31 @@ QNN_API qnn_status_t qnn_dequantize(const void* in, qnn_dtype_t in_dtype, float*
                             int32_t ndim, int32_t axis, const float* scales, const int32_t* zero_points,
                             int32_t n_params, qnn_stream_t stream);
 
+/* Host-buffer forms of quantize / dequantize: the end-to-end entry and exit of a network whose
+ * input and output live in host memory (BASELINE configs[4]'s f32 images in, logits out).
+ *
+ * qnn_quantize_host: `host_in` is page-locked host memory (cudaHostAlloc / cudaHostRegister /
+ *   torch pin_memory) holding the f32 tensor.  The call enqueues the host->device copy of
+ *   prod(shape) * 4 bytes into `staging` (device memory, caller-owned, at least that size) on
+ *   `copy_stream` (a copy engine: it runs alongside kernels on other streams), makes `stream` wait
+ *   for that copy, then quantizes staging -> `out` (device) on `stream`, exactly as qnn_quantize.
+ *   The caller orders `copy_stream` after the previous reader of `staging` (double buffering:
+ *   two staging buffers, copy_stream waiting on an event recorded after the quantize that last
+ *   read the buffer); copy_stream may equal stream (no overlap).
+ * qnn_dequantize_host: `host_out` is page-locked host memory; the dequantize kernel writes the
+ *   f32 result straight into it through its mapped device address (zero-copy over PCIe), so the
+ *   values are on the host once `stream` passes the call.  Otherwise exactly qnn_dequantize.
+ * Errors: QNN_ERR_INVALID_VALUE when the host pointer is not page-locked host memory (pageable
+ * memory cannot be read or written by the device asynchronously) or when `staging` is null;
+ * QNN_ERR_CUDA on a failed copy enqueue.  Enqueue-only. */
+QNN_API qnn_status_t qnn_quantize_host(const float* host_in, float* staging, void* out, qnn_dtype_t out_dtype,
+                               const int64_t* shape, int32_t ndim, int32_t axis, const float* scales,
+                               const int32_t* zero_points, int32_t n_params, qnn_stream_t copy_stream,
+                               qnn_stream_t stream);
+QNN_API qnn_status_t qnn_dequantize_host(const void* in, qnn_dtype_t in_dtype, float* host_out, const int64_t* shape,
+                                 int32_t ndim, int32_t axis, const float* scales, const int32_t* zero_points,
+                                 int32_t n_params, qnn_stream_t stream);
+
 /* -------------------------------------------------------------------------------------------
  * Inter-layer glue (the paper's framework operators quantized_add and
  * pooling).

@@ -10,5 +10,5 @@ The compute lives in ``libqnn.so`` (CUDA for sm_100a, C ABI in
 """
 from . import qnn  # noqa: F401
 from .qnn import (PackedConv2d, PackedDense, QnnError, lib, qnn_add, qnn_conv2d, qnn_dense,  # noqa: F401
-                  qnn_depthwise_conv2d, qnn_dequantize, qnn_derive_multiplier, qnn_pool2d, qnn_quantize,
-                  qnn_requantize)
+                  qnn_depthwise_conv2d, qnn_dequantize, qnn_dequantize_host, qnn_derive_multiplier, qnn_pool2d,
+                  qnn_quantize, qnn_quantize_host, qnn_requantize)

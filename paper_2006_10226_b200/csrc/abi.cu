@@ -1411,6 +1411,62 @@ qnn_status_t qnn_dequantize(const void* in, qnn_dtype_t in_dtype, float* out, co
                       (cudaStream_t)stream);
 }
 
+// page-locked host memory -> the device address kernels and copies use (UVA: usually the same
+// pointer); nullptr for pageable or device memory
+static void* pinned_device_ptr(const void* host) {
+  cudaPointerAttributes at{};
+  if (!host || cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return at.devicePointer;
+}
+
+qnn_status_t qnn_quantize_host(const float* host_in, float* staging, void* out, qnn_dtype_t out_dtype,
+                               const int64_t* shape, int32_t ndim, int32_t axis, const float* scales,
+                               const int32_t* zero_points, int32_t n_params, qnn_stream_t copy_stream,
+                               qnn_stream_t stream) {
+  if (!shape || ndim < 1 || ndim > 8 || !staging) return QNN_ERR_INVALID_VALUE;
+  int64_t count = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (shape[i] < 0) return QNN_ERR_INVALID_VALUE;
+    count *= shape[i];
+  }
+  if (count > 0 && !pinned_device_ptr(host_in)) return QNN_ERR_INVALID_VALUE;
+  cudaStream_t cs = (cudaStream_t)copy_stream, s = (cudaStream_t)stream;
+  if (count > 0) {
+    if (cudaMemcpyAsync(staging, host_in, (size_t)count * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+      return QNN_ERR_CUDA;
+    if (cs != s) {
+      // the quantize waits for the copy: one event per device, recorded and waited back to back
+      // (a wait binds to the record that precedes it, so reuse is safe); serialised per process
+      static std::mutex mu;
+      static cudaEvent_t ev[64] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev >= 64) return QNN_ERR_UNSUPPORTED;
+      std::lock_guard<std::mutex> lk(mu);
+      if (!ev[dev] && cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming) != cudaSuccess) return QNN_ERR_CUDA;
+      if (cudaEventRecord(ev[dev], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[dev], 0) != cudaSuccess)
+        return QNN_ERR_CUDA;
+    }
+  }
+  return quant_common(staging, out, out_dtype, shape, ndim, axis, scales, zero_points, n_params, true, s);
+}
+
+qnn_status_t qnn_dequantize_host(const void* in, qnn_dtype_t in_dtype, float* host_out, const int64_t* shape,
+                                 int32_t ndim, int32_t axis, const float* scales, const int32_t* zero_points,
+                                 int32_t n_params, qnn_stream_t stream) {
+  if (!shape || ndim < 1 || ndim > 8) return QNN_ERR_INVALID_VALUE;
+  int64_t count = 1;
+  for (int i = 0; i < ndim; ++i) count *= shape[i] < 0 ? 0 : shape[i];
+  float* dptr = static_cast<float*>(pinned_device_ptr(host_out));
+  if (count > 0 && !dptr) return QNN_ERR_INVALID_VALUE;
+  return quant_common(in, dptr, in_dtype, shape, ndim, axis, scales, zero_points, n_params, false,
+                      (cudaStream_t)stream);
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------- glue

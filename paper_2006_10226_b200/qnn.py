@@ -33,7 +33,8 @@ EXPORTED = ["qnn_status_string", "qnn_launch_counter", "qnn_launch_counter_reset
             "qnn_conv2d_prepack_size", "qnn_conv2d_prepack", "qnn_conv2d_workspace_size", "qnn_conv2d_packed",
             "qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense_prepack_size", "qnn_dense_prepack",
             "qnn_dense_workspace_size", "qnn_dense_packed", "qnn_dense", "qnn_requantize", "qnn_quantize",
-            "qnn_dequantize", "qnn_add", "qnn_pool2d", "qnn_conv2d_packed_add"]
+            "qnn_dequantize", "qnn_add", "qnn_pool2d", "qnn_conv2d_packed_add", "qnn_quantize_host",
+            "qnn_dequantize_host"]
 
 
 class QnnError(RuntimeError):
@@ -106,6 +107,10 @@ def lib() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
             L.qnn_dequantize.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(i64), i32, i32,
                                          ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
+            L.qnn_quantize_host.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.POINTER(i64), i32, i32,
+                                            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp, vp]
+            L.qnn_dequantize_host.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(i64), i32, i32,
+                                              ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32), i32, vp]
             f32 = ctypes.c_float
             L.qnn_add.argtypes = [vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32,
                                   i64, ctypes.c_int, i32, vp]
@@ -380,6 +385,50 @@ def qnn_dequantize(q: torch.Tensor, scales, zero_points, axis=-1, out=None, stre
     _check(lib().qnn_dequantize(_dev(q, "q"), _TORCH_DT[q.dtype], _dev(out, "out"), shp, nd, int(axis), sc, zp,
                                 len(sc), ctypes.c_void_p(_stream(stream))), "qnn_dequantize")
     return out
+
+
+def _pinned(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_pinned():
+        raise QnnError(f"{name} must be a pinned (page-locked) host tensor")
+    if not t.is_contiguous():
+        raise QnnError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _params(scales, zero_points):
+    sc, zp = _floats(scales), _ints(zero_points)
+    if len(zp) == 1 and len(sc) > 1:
+        zp = _ints([zp[0]] * len(sc))
+    if len(sc) == 1 and len(zp) > 1:
+        sc = _floats([sc[0]] * len(zp))
+    return sc, zp
+
+
+def qnn_quantize_host(x_host: torch.Tensor, staging: torch.Tensor, out: torch.Tensor, scales, zero_points,
+                      out_dtype="u8", axis=-1, copy_stream=None, stream=None):
+    """qnn_quantize_host: pinned host f32 -> (copy engine, copy_stream) staging -> quantize -> out
+    on stream (the C-ABI entry of an end-to-end step; see include/qnn.h for the ordering rules)."""
+    if staging.numel() < x_host.numel() or staging.dtype != torch.float32:
+        raise QnnError("staging must be a float32 CUDA tensor at least as large as the input")
+    shp, nd = _shape(x_host)
+    sc, zp = _params(scales, zero_points)
+    _check(lib().qnn_quantize_host(_pinned(x_host, "x_host"), _dev(staging, "staging"), _dev(out, "out"),
+                                   _dtcode(out_dtype), shp, nd, int(axis), sc, zp, len(sc),
+                                   ctypes.c_void_p(_stream(copy_stream)), ctypes.c_void_p(_stream(stream))),
+           "qnn_quantize_host")
+    return out
+
+
+def qnn_dequantize_host(q: torch.Tensor, out_host: torch.Tensor, scales, zero_points, axis=-1, stream=None):
+    """qnn_dequantize_host: the dequantize kernel writes straight into pinned host memory."""
+    if out_host.dtype != torch.float32 or out_host.numel() != q.numel():
+        raise QnnError("out_host must be a float32 tensor with q's element count")
+    shp, nd = _shape(q)
+    sc, zp = _params(scales, zero_points)
+    _check(lib().qnn_dequantize_host(_dev(q, "q"), _TORCH_DT[q.dtype], _pinned(out_host, "out_host"), shp, nd,
+                                     int(axis), sc, zp, len(sc), ctypes.c_void_p(_stream(stream))),
+           "qnn_dequantize_host")
+    return out_host
 
 
 # --------------------------------------------------------------------------- glue (SURVEY §8f f1)

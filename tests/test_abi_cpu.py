@@ -26,8 +26,9 @@ def _declared_symbols():
 
 def test_header_declares_abi():
     syms = _declared_symbols()
-    assert len(syms) == 21
-    for s in ("qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense", "qnn_requantize", "qnn_quantize", "qnn_dequantize"):
+    assert len(syms) == 23
+    for s in ("qnn_conv2d", "qnn_depthwise_conv2d", "qnn_dense", "qnn_requantize", "qnn_quantize", "qnn_dequantize",
+              "qnn_quantize_host", "qnn_dequantize_host"):
         assert s in syms
 
 
