@@ -531,10 +531,14 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   }
   // a_rows: stride-1 im2col convs with resident weights load the input rows a tile touches
   // once per channel chunk and address every tap through the MMA descriptor (no per-tap
-  // im2col TMA); QNN_NO_AROWS=1 keeps the im2col path (A/B measurements)
+  // im2col TMA); QNN_NO_AROWS=1 keeps the im2col path (A/B measurements).  Its epilogue
+  // stores directly (no TMA-store staging), and those 32 KB are what let the weights of a
+  // 128 x 128 x 3 x 3 layer (147 KB) stay resident beside two staged-row stages: the
+  // streamed-weight im2col plan of such a layer is bound by the L2 -> SM feed (every tile
+  // re-reads all weights and 9 im2col boxes).
   static const bool no_arows = std::getenv("QNN_NO_AROWS") != nullptr;
   if (!no_arows && pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && d->stride_h == 1 && d->stride_w == 1 &&
-      d->dil_h == 1 && d->dil_w == 1 && pl.num_n == 1 && pl.b_res_kb > 0 && d->C % pl.BK == 0) {
+      d->dil_h == 1 && d->dil_w == 1 && pl.num_n == 1 && d->C % pl.BK == 0) {
     const int Wp = pl.Q + d->S - 1;
     const long long flat = (long long)pl.P * Wp;
     const int T = (int)((flat + kGemmBM - 1) / kGemmBM);
@@ -547,10 +551,18 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     const int ncls = pl.ct.ncr * pl.ct.ncc;
     const int num_kb = d->R * d->S * pl.nchunks;
     if (Wp <= 256 && nri <= 256 && a_stage <= 96 * 1024) {
-      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts);
-      if (st >= 2 &&
-          gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts) <= 227 * 1024) {
+      // (stage count as if the staging region were there when that leaves >= 2 stages: deeper
+      // rings measured no faster on ResNet-50 layer1; without it only when it is what fits)
+      int st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts, true);
+      if (st < 2 || gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts,
+                                    true) > 227 * 1024)
+        st = gemm_max_stages(pl.BK, pl.BN, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts, false);
+      static const int arows_cap = std::getenv("QNN_AROWS_STAGES") ? std::atoi(std::getenv("QNN_AROWS_STAGES")) : 0;
+      if (arows_cap >= 2 && st > arows_cap) st = arows_cap;   // (A/B measurements of the ring depth)
+      if (st >= 2 && gemm_smem_bytes(pl.BK, pl.BN, st, ncls, num_kb * bparts, d->R * d->S, 0, (int)a_stage, bparts,
+                                     false) <= 227 * 1024) {
         pl.a_rows = true;
+        pl.b_res_kb = num_kb;
         pl.a_Wp = Wp;
         pl.a_T = T;
         pl.a_nri = nri;
@@ -1149,6 +1161,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   ep.ncc = pl.ct.ncc;
   ep.ncls = pl.ct.ncr * pl.ct.ncc;
   ep.tma_store = tma_store;
+  p.out_staging = tma_store ? 1 : 0;   // a_rows plans are sized without the staging region
   ep.rowsum = rowsum;
   ep.zpW = pl.wsplit ? 0 : d->kernel_zero_point;
   ep.out = output;

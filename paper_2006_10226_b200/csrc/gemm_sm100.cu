@@ -11,17 +11,21 @@ namespace qnn {
 // Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
 // commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes,
-                       int a_stage_bytes, int bparts) {
+                       int a_stage_bytes, int bparts, bool out_staging) {
   // (bparts = 2: split weights, two B k-blocks per A k-block; b_res_kb then counts both parts)
   const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK * bparts;
   const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * (b / bparts) : stages * (a + b * kps);
-  return 1024 + ring + (size_t)stages * raw_bytes + kStageOutBytes + kParamBytes + off_table_bytes(ncls, BN) + 512;
+  return 1024 + ring + (size_t)stages * raw_bytes + (out_staging ? kStageOutBytes : 0) + kParamBytes +
+         off_table_bytes(ncls, BN) + 512;
 }
 
-int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes, int bparts) {
+int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes, int bparts,
+                    bool out_staging) {
   const size_t budget = 227 * 1024;
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes, bparts) > budget) --s;
+  while (s > 2 &&
+         gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes, bparts, out_staging) > budget)
+    --s;
   return s;
 }
 

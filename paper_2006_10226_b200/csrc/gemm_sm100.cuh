@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sOut = sRaw + (size_t)stages * p.a_raw_bytes;
   const bool tracing = kInstrument && p.trace != nullptr && blockIdx.x == 0;
   const int dbg = kInstrument ? p.dbg : 0;
-  int2* sMT = reinterpret_cast<int2*>(sOut + kStageOutBytes);          // {M, t} per column
+  int2* sMT = reinterpret_cast<int2*>(sOut + (p.out_staging ? kStageOutBytes : 0));   // {M, t} per column
   int32_t* sCC = reinterpret_cast<int32_t*>(sMT + 256);               // c per column
   int32_t* sOff = sCC + 512;
   const int ncls = HAS_CLS ? p.e.ncls : 1;
@@ -813,7 +813,7 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   }
   constexpr int bparts = SPLIT ? 2 : 1;
   const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb * bparts : 0,
-                                      p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts);
+                                      p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts, p.out_staging != 0);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
   count_launch();

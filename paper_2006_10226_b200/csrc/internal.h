@@ -141,6 +141,7 @@ struct GemmParams {
   FastDiv fdT, fdWp;
   GemmEpilogue e;
   int wsplit; // weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction)
+  int out_staging;  // the epilogue's TMA-store staging region is allocated (0: direct stores only)
 };
 
 constexpr int kGemmBM = 128;
@@ -169,10 +170,11 @@ __host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles, int nepi =
 }
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
+// out_staging = false: no TMA-store staging region (plans whose epilogue stores directly)
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0,
-                       int a_stage_bytes = 0, int bparts = 1);
+                       int a_stage_bytes = 0, int bparts = 1, bool out_staging = true);
 int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0, int a_stage_bytes = 0,
-                    int bparts = 1);
+                    int bparts = 1, bool out_staging = true);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 cudaError_t launch_gemm_split(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
