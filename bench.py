@@ -678,13 +678,58 @@ def oracle_full_forward(m, n_img: int = 1):
     return orc.dequantize(acc, scale, [0], axis=-1)
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_single_thread_rates():
+    """the oracle's single-thread rate on C1 (the 3x3 16->16 conv at 8x8, batch 1)
+    and C4-512 (qnn.dense 512^3), int64 MAC/s, each repeated for about a second."""
+    import oracle as orc
+    from workloads import gen
+    n0 = orc.num_threads()
+    orc.set_num_threads(1)
+    try:
+        c = gen.conv_case(101, 1, 16, 8, 8, 16, 3, 3, (1, 1), (1, 1, 1, 1), relu=False, zp_A=128, zp_out=128)
+        macs1 = 64 * 16 * 144
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < 1.0:
+            orc.qnn_conv2d(c.nchw(), c.oihw(), c.zp_A, c.zp_W, c.s_A, c.s_W, c.bias, c.out_params(), c.stride, c.pad)
+            reps += 1
+        dt1 = (time.perf_counter() - t0) / reps
+        d = gen.dense_case(3512, 512, 512, 512)
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < 1.0 or reps == 0:
+            orc.qnn_dense(d.A, d.W, d.zp_A, d.zp_W, d.s_A, d.s_W, d.bias, d.out_params())
+            reps += 1
+        dt4 = (time.perf_counter() - t0) / reps
+    finally:
+        orc.set_num_threads(n0)
+    return {"C1_us": round(dt1 * 1e6, 1), "C1_gmacs": round(macs1 / dt1 / 1e9, 3),
+            "C4_512_ms": round(dt4 * 1e3, 2), "C4_512_gmacs": round(512 ** 3 / dt4 / 1e9, 3), "threads": 1}
+
+
 def cpu_baseline(model, n_img: int = 1):
     import oracle as orc
     t0 = time.perf_counter()
     oracle_forward(model, n_img)
     dt = time.perf_counter() - t0
-    return {"value": n_img / dt, "unit": "images/s", "cores": orc.num_threads(), "kind": "oracle",
-            "sample": f"{n_img} image(s) through the full stack (quantize, 53 conv, fc, dequantize), {dt:.1f} s"}
+    macs = sum(sp.N * sp.P * sp.Q * sp.K * sp.R * sp.S * sp.C for sp in model["specs"]) / max(1, model["specs"][0].N)
+    out = {"value": n_img / dt, "unit": "images/s", "cores": orc.num_threads(), "kind": "oracle",
+           "sample": f"{n_img} image(s) through the full stack (quantize, 53 conv, fc, dequantize), {dt:.1f} s",
+           "gmacs": round(n_img * macs / dt / 1e9, 2), "cpu": _cpu_model(),
+           "affinity_cores": len(os.sched_getaffinity(0))}
+    try:
+        out["single_thread"] = oracle_single_thread_rates()
+    except Exception as e:    # a timing extra: never fail the bench line for it
+        out["single_thread"] = {"error": str(e)[:200]}
+    return out
 
 
 def run_reference(args, rank, world):

@@ -72,6 +72,7 @@ def lib():
             L.oracle_quantize.argtypes = [vp, i64, i64, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int, vp]
             L.oracle_dequantize.argtypes = [vp, ctypes.c_int, i64, i64, ctypes.c_int, vp, vp, ctypes.c_int, vp]
             L.oracle_num_threads.restype = ctypes.c_int
+            L.oracle_set_num_threads.argtypes = [ctypes.c_int]
             f32 = ctypes.c_float
             L.oracle_add.argtypes = [vp, ctypes.c_int, f32, i32, vp, ctypes.c_int, f32, i32, i64, f32, i32,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
@@ -92,6 +93,11 @@ def _dt_of(a: np.ndarray) -> str:
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """Thread count of the oracle's later OpenMP regions (timing only; results do not depend on it)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 # --------------------------------------------------------------------------- #

@@ -465,11 +465,15 @@ void oracle_pool2d(const void* in, int dt, int is_avg, int N, int C, int H, int 
 }
 
 int oracle_num_threads(void);
+void oracle_set_num_threads(int n);
 }  /* extern "C" */
 
 #ifdef _OPENMP
 #include <omp.h>
 extern "C" int oracle_num_threads(void) { return omp_get_max_threads(); }
+// thread count of later parallel regions (timing only: the single-thread oracle rate)
+extern "C" void oracle_set_num_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
 #else
 extern "C" int oracle_num_threads(void) { return 1; }
+extern "C" void oracle_set_num_threads(int) {}
 #endif
