@@ -23,6 +23,11 @@ namespace qnn {
 static thread_local uint64_t g_launches = 0;
 void count_launch(int n) { g_launches += (uint64_t)n; }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("QNN_NO_PDL") == nullptr;
+  return on;
+}
+
 static int sm_count() {
   static int cached[64] = {0};
   int dev = 0;

@@ -174,6 +174,14 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+// Programmatic dependent launch (PDL).  A kernel launched with programmatic stream
+// serialization (launch_pdl) may start while the previous kernel of the stream is finishing:
+// pdl_wait() blocks until that kernel has completed and its writes are visible (it returns at
+// once in a normal launch), so everything before it may touch only constant data (packed
+// weights, parameters).  pdl_trigger() lets the next kernel of the stream launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32 (kind::i8)
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {

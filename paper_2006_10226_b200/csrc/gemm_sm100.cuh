@@ -195,6 +195,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (tracing && threadIdx.x == 0) trace_at(p.trace, 6001);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();                        // the next layer's kernel may launch and run its prologue
+  if (warp != kProdWarp) pdl_wait();    // (the producer waits after issuing the resident weights)
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
   // tile t = m_blk * nn + n_blk, visited t = blockIdx.x, += gridDim.x: (m_blk, n_blk) advanced without division
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       __syncwarp();
     }
+    pdl_wait();   // activations are the previous kernel's output
     int stage = 0, it_p = 0;
     uint32_t phase = 0;
     const bool skip_a = dbg & 4;
@@ -815,9 +818,10 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb * bparts : 0,
                                       p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts, p.out_staging != 0);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  kern<<<grid, kGemmThreads, smem, stream>>>(tmA, tmB, tmC[0], tmC[1], tmC[2], tmC[3], p);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, stream, tmA, tmB, tmC[0], tmC[1], tmC[2],
+                             tmC[3], p);
   count_launch();
-  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   static const bool trace_err = std::getenv("QNN_PLAN_TRACE") != nullptr;
   if (e != cudaSuccess && trace_err)
     std::fprintf(stderr, "[qnn gemm] launch failed: %s (grid %d, %d threads, %zu B smem)\n", cudaGetErrorString(e),

@@ -268,6 +268,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+  pdl_trigger();                        // the next layer's kernel may launch and run its prologue
+  if (warp != kProdWarp) pdl_wait();    // (the producer waits after issuing the resident weights)
 
   if (warp == kProdWarp) {
     const bool leader = elect_one();
@@ -277,6 +279,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       for (int kb = 0; kb < num_kb * wparts; ++kb)
         tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
     }
+    pdl_wait();   // activations are the previous kernel's output
     int stage = 0;
     uint32_t phase = 0;
     if (build) {
@@ -625,9 +628,9 @@ cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
       if (e != cudaSuccess) return e;                                                                      \
       if (dev < 64) attr_done[dev] = 1;                                                                    \
     }                                                                                                      \
-    kern<<<grid, kTThreads, smem, stream>>>(tmX, tmW, tmC, tmR, p);                                        \
+    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kTThreads), smem, stream, tmX, tmW, tmC, tmR, p);    \
     count_launch();                                                                                        \
-    const cudaError_t e = cudaGetLastError();                                                              \
+    if (e == cudaSuccess) e = cudaGetLastError();                                                          \
     if (e != cudaSuccess && std::getenv("QNN_PLAN_TRACE"))                                                 \
       std::fprintf(stderr, "[qnn gemm_t] launch failed: %s\n", cudaGetErrorString(e));                    \
     return e;                                                                                              \

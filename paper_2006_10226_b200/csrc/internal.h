@@ -144,6 +144,26 @@ struct GemmParams {
   int out_staging;  // the epilogue's TMA-store staging region is allocated (0: direct stores only)
 };
 
+// Launch with programmatic stream serialization (PDL) so the kernel's prologue (barrier init,
+// TMEM allocation, descriptor prefetch, resident-weight loads) overlaps the previous kernel's
+// tail; the kernel must call pdl_wait() before it reads or writes activations.  QNN_NO_PDL=1
+// launches normally (A/B measurements).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 constexpr int kGemmBM = 128;
 constexpr int kGemmEpiWarps = 16;
 // 20 warps: the register file is allocated per 4-warp group, so 18 warps would cost as much
