@@ -52,6 +52,8 @@ struct VecLoad<1> {
 
 template <int VEC>
 __global__ void __launch_bounds__(256) depthwise_kernel(const __grid_constant__ DwParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const int ngroups = p.C / VEC;
   const long long total = (long long)p.N * p.P * p.Q * ngroups;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -118,11 +120,11 @@ cudaError_t launch_depthwise(const DwParams& p, cudaStream_t s) {
   const long long want = (total + threads - 1) / threads;
   const int blocks = (int)std::max<long long>(1, std::min<long long>(want, (long long)sms * 8));
   if (vec == 16)
-    depthwise_kernel<16><<<blocks, threads, 0, s>>>(p);
+    launch_pdl(depthwise_kernel<16>, dim3(blocks), dim3(threads), 0, s, p);
   else if (vec == 4)
-    depthwise_kernel<4><<<blocks, threads, 0, s>>>(p);
+    launch_pdl(depthwise_kernel<4>, dim3(blocks), dim3(threads), 0, s, p);
   else
-    depthwise_kernel<1><<<blocks, threads, 0, s>>>(p);
+    launch_pdl(depthwise_kernel<1>, dim3(blocks), dim3(threads), 0, s, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -302,6 +304,8 @@ __device__ __forceinline__ void dw3_items(const DwParams& p, int c0, int first, 
 
 template <int SH, int MODE, int CLAMP, bool S8OUT, bool ASIGNED>
 __global__ void __launch_bounds__(256, 2) depthwise3_kernel(const __grid_constant__ DwParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const int G = p.C >> 2;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nthreads = (long long)gridDim.x * blockDim.x;
@@ -382,7 +386,7 @@ bool launch_depthwise3(const DwParams& p, int clamp, cudaStream_t s) {
   const bool s8 = p.out_dtype == DT_S8;
 #define QNN_DW3(SH_, M_, C_, S_, A_)                                                                      \
   if (p.sh == SH_ && p.mode == M_ && clamp == C_ && s8 == S_ && (p.a_signed != 0) == A_) {               \
-    depthwise3_kernel<SH_, M_, C_, S_, A_><<<(int)blocks, 256, 0, s>>>(q);                                  \
+    launch_pdl(depthwise3_kernel<SH_, M_, C_, S_, A_>, dim3((int)blocks), dim3(256), 0, s, q);                                  \
     count_launch();                                                                                        \
     return true;                                                                                           \
   }

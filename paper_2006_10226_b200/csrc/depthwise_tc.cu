@@ -82,6 +82,8 @@ size_t dwtc_param_bytes(int ncls) { return (size_t)kDwSets * (256 + 128 + (size_
 template <int MODE, bool CLAMP, bool S8OUT>
 __global__ void __launch_bounds__(kDwThreads, 1)
     depthwise_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ DwTcParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;                                           // p.stages x p.stage_bytes
@@ -337,7 +339,7 @@ static cudaError_t dwtc_launch_variant(const CUtensorMap& tmA, const DwTcParams&
     if (e != cudaSuccess) return e;
     if (dev < 64) attr_done[dev] = 1;
   }
-  kern<<<grid, kDwThreads, dwtc_smem_bytes(p.stages, p.stage_bytes, p.ncls), s>>>(tmA, p);
+  launch_pdl(kern, dim3(grid), dim3(kDwThreads), dwtc_smem_bytes(p.stages, p.stage_bytes, p.ncls), s, tmA, p);
   count_launch();
   return cudaGetLastError();
 }

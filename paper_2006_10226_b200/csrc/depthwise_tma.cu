@@ -144,6 +144,8 @@ __device__ __forceinline__ void dwt_band(const DwParams& p, const uint8_t* __res
 template <int SH, int CLAMP, bool S8OUT, bool ASIGNED>
 __global__ void __launch_bounds__(kDwtThreads, 3) dw3_tma_kernel(const __grid_constant__ CUtensorMap tm,
                                                                  const __grid_constant__ DwParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   extern __shared__ __align__(128) uint8_t dwt_smem[];
   __shared__ __align__(8) uint64_t full[2];
   const int CS = p.dwt_cs, G = CS >> 2;
@@ -270,7 +272,7 @@ cudaError_t launch_depthwise_tma(const CUtensorMap& tm, const DwParams& p, int c
     auto kern = dw3_tma_kernel<SH_, C_, S_, A_>;                                                            \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                                          \
-    kern<<<(int)grid, kDwtThreads, smem, s>>>(tm, p);                                                        \
+    launch_pdl(kern, dim3((int)grid), dim3(kDwtThreads), smem, s, tm, p);                                                        \
     count_launch();                                                                                          \
     return cudaGetLastError();                                                                               \
   }

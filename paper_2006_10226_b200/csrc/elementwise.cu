@@ -86,6 +86,8 @@ __device__ __forceinline__ int grid_threads() { return gridDim.x * blockDim.x; }
 // ------------------------------------------------------------------ requantize
 template <int IN, int OUT>
 __global__ void __launch_bounds__(256) requantize_kernel(const __grid_constant__ RequantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   __shared__ int32_t s_mult[kMaxChanParams];
   __shared__ int8_t s_rsh[kMaxChanParams];
   for (int c = threadIdx.x; c < p.nch; c += blockDim.x) {
@@ -133,9 +135,9 @@ static int ew_blocks(long long work_items) {
 template <int IN>
 static void dispatch_rq_out(const RequantParams& p, int blocks, cudaStream_t s) {
   switch (p.out_dt) {
-    case DT_S8: requantize_kernel<IN, DT_S8><<<blocks, 256, 0, s>>>(p); break;
-    case DT_U8: requantize_kernel<IN, DT_U8><<<blocks, 256, 0, s>>>(p); break;
-    default: requantize_kernel<IN, DT_S32><<<blocks, 256, 0, s>>>(p); break;
+    case DT_S8: launch_pdl(requantize_kernel<IN, DT_S8>, dim3(blocks), dim3(256), 0, s, p); break;
+    case DT_U8: launch_pdl(requantize_kernel<IN, DT_U8>, dim3(blocks), dim3(256), 0, s, p); break;
+    default: launch_pdl(requantize_kernel<IN, DT_S32>, dim3(blocks), dim3(256), 0, s, p); break;
   }
 }
 
@@ -164,6 +166,8 @@ __device__ __forceinline__ int32_t quant1(float x, float s, int32_t zp, int32_t 
 
 template <int OUT>
 __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QuantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   __shared__ float s_sc[kMaxQuantParams];
   __shared__ int32_t s_zp[kMaxQuantParams];
   for (int c = threadIdx.x; c < p.nch; c += blockDim.x) {
@@ -211,9 +215,9 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
 static cudaError_t launch_quantize_generic(const QuantParams& p, cudaStream_t s) {
   const int blocks = ew_blocks((p.count + 15) / 16);
   if (p.q_dt == DT_S8)
-    quantize_kernel<DT_S8><<<blocks, 256, 0, s>>>(p);
+    launch_pdl(quantize_kernel<DT_S8>, dim3(blocks), dim3(256), 0, s, p);
   else
-    quantize_kernel<DT_U8><<<blocks, 256, 0, s>>>(p);
+    launch_pdl(quantize_kernel<DT_U8>, dim3(blocks), dim3(256), 0, s, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -233,6 +237,8 @@ __device__ __forceinline__ float dequant1(int64_t q, float s, int32_t zp) {
 
 template <int IN>
 __global__ void __launch_bounds__(256) dequantize_kernel(const __grid_constant__ QuantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   __shared__ float s_sc[kMaxQuantParams];
   __shared__ int32_t s_zp[kMaxQuantParams];
   for (int c = threadIdx.x; c < p.nch; c += blockDim.x) {
@@ -275,9 +281,9 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const __grid_constant__
 static cudaError_t launch_dequantize_generic(const QuantParams& p, cudaStream_t s) {
   const int blocks = ew_blocks((p.count + 15) / 16);
   switch (p.q_dt) {
-    case DT_S8: dequantize_kernel<DT_S8><<<blocks, 256, 0, s>>>(p); break;
-    case DT_U8: dequantize_kernel<DT_U8><<<blocks, 256, 0, s>>>(p); break;
-    default: dequantize_kernel<DT_S32><<<blocks, 256, 0, s>>>(p); break;
+    case DT_S8: launch_pdl(dequantize_kernel<DT_S8>, dim3(blocks), dim3(256), 0, s, p); break;
+    case DT_U8: launch_pdl(dequantize_kernel<DT_U8>, dim3(blocks), dim3(256), 0, s, p); break;
+    default: launch_pdl(dequantize_kernel<DT_S32>, dim3(blocks), dim3(256), 0, s, p); break;
   }
   count_launch();
   return cudaGetLastError();
@@ -452,6 +458,8 @@ __device__ __forceinline__ int32_t rq_fast(int32_t x, const RqCh& q, int32_t zp_
 
 template <int IN, int OUT, int MODE, int CM>
 __global__ void __launch_bounds__(256) requantize_fast_kernel(const __grid_constant__ RequantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const long long nthreads = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (CM == CM_LAST) {
@@ -549,9 +557,9 @@ static int fast_blocks(long long vectors, int cm, int cext) {
 
 template <int IN, int OUT, int MODE>
 static void launch_rq_cm(const RequantParams& p, int cm, int blocks, cudaStream_t s) {
-  if (cm == CM_TENSOR) requantize_fast_kernel<IN, OUT, MODE, CM_TENSOR><<<blocks, 256, 0, s>>>(p);
-  else if (cm == CM_VEC) requantize_fast_kernel<IN, OUT, MODE, CM_VEC><<<blocks, 256, 0, s>>>(p);
-  else requantize_fast_kernel<IN, OUT, MODE, CM_LAST><<<blocks, 256, 0, s>>>(p);
+  if (cm == CM_TENSOR) launch_pdl(requantize_fast_kernel<IN, OUT, MODE, CM_TENSOR>, dim3(blocks), dim3(256), 0, s, p);
+  else if (cm == CM_VEC) launch_pdl(requantize_fast_kernel<IN, OUT, MODE, CM_VEC>, dim3(blocks), dim3(256), 0, s, p);
+  else launch_pdl(requantize_fast_kernel<IN, OUT, MODE, CM_LAST>, dim3(blocks), dim3(256), 0, s, p);
 }
 template <int IN, int OUT>
 static void launch_rq_mode(const RequantParams& p, int cm, int blocks, cudaStream_t s) {
@@ -605,6 +613,8 @@ __device__ __forceinline__ int32_t quant_fast(float x, float s, float rs, float 
 }
 template <int OUT, int CM>
 __global__ void __launch_bounds__(256) quantize_fast_kernel(const __grid_constant__ QuantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const long long nthreads = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const float* in = reinterpret_cast<const float*>(p.in);
@@ -667,9 +677,9 @@ cudaError_t launch_quantize(const QuantParams& p, cudaStream_t s) {
   if (cm < 0) return launch_quantize_generic(p, s);
   const int blocks = fast_blocks(p.count / 16, cm, p.cext);
 #define QNN_QF(OUT_)                                                                        \
-  if (cm == CM_TENSOR) quantize_fast_kernel<OUT_, CM_TENSOR><<<blocks, 256, 0, s>>>(p);     \
-  else if (cm == CM_VEC) quantize_fast_kernel<OUT_, CM_VEC><<<blocks, 256, 0, s>>>(p);      \
-  else quantize_fast_kernel<OUT_, CM_LAST><<<blocks, 256, 0, s>>>(p);
+  if (cm == CM_TENSOR) launch_pdl(quantize_fast_kernel<OUT_, CM_TENSOR>, dim3(blocks), dim3(256), 0, s, p);     \
+  else if (cm == CM_VEC) launch_pdl(quantize_fast_kernel<OUT_, CM_VEC>, dim3(blocks), dim3(256), 0, s, p);      \
+  else launch_pdl(quantize_fast_kernel<OUT_, CM_LAST>, dim3(blocks), dim3(256), 0, s, p);
   if (p.q_dt == DT_S8) {
     QNN_QF(DT_S8)
   } else {
@@ -683,6 +693,8 @@ cudaError_t launch_quantize(const QuantParams& p, cudaStream_t s) {
 // ---- dequantize (8-bit): x = fl32((q - zp) * s), one rounding of an exact product
 template <int IN, int CM>
 __global__ void __launch_bounds__(256) dequantize_fast_kernel(const __grid_constant__ QuantParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const long long nthreads = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   float* out = reinterpret_cast<float*>(p.out);
@@ -742,9 +754,9 @@ cudaError_t launch_dequantize(const QuantParams& p, cudaStream_t s) {
   if (cm < 0) return launch_dequantize_generic(p, s);
   const int blocks = fast_blocks(p.count / 16, cm, p.cext);
 #define QNN_DQ(IN_)                                                                          \
-  if (cm == CM_TENSOR) dequantize_fast_kernel<IN_, CM_TENSOR><<<blocks, 256, 0, s>>>(p);     \
-  else if (cm == CM_VEC) dequantize_fast_kernel<IN_, CM_VEC><<<blocks, 256, 0, s>>>(p);      \
-  else dequantize_fast_kernel<IN_, CM_LAST><<<blocks, 256, 0, s>>>(p);
+  if (cm == CM_TENSOR) launch_pdl(dequantize_fast_kernel<IN_, CM_TENSOR>, dim3(blocks), dim3(256), 0, s, p);     \
+  else if (cm == CM_VEC) launch_pdl(dequantize_fast_kernel<IN_, CM_VEC>, dim3(blocks), dim3(256), 0, s, p);      \
+  else launch_pdl(dequantize_fast_kernel<IN_, CM_LAST>, dim3(blocks), dim3(256), 0, s, p);
   if (p.q_dt == DT_S8) {
     QNN_DQ(DT_S8)
   } else {

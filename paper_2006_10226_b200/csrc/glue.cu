@@ -41,6 +41,8 @@ __device__ __forceinline__ int32_t rq_small(int32_t xz, int32_t M, int rsh, int 
 // --------------------------------------------------------------------------------- qnn.add
 template <bool AS8, bool BS8, bool OS8>
 __global__ void __launch_bounds__(256) add_kernel(const __grid_constant__ AddParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const long long nthreads = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nvec = p.vec ? p.count >> 4 : 0;
@@ -80,7 +82,7 @@ cudaError_t launch_add(const AddParams& p, cudaStream_t s) {
   const long long work = p.vec ? (p.count + 15) / 16 : p.count;
   const int blocks = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)sms * 8));
 #define QNN_ADD(A_, B_, O_) \
-  if (p.a_s8 == A_ && p.b_s8 == B_ && p.o_s8 == O_) add_kernel<A_, B_, O_><<<blocks, 256, 0, s>>>(p);
+  if (p.a_s8 == A_ && p.b_s8 == B_ && p.o_s8 == O_) launch_pdl(add_kernel<A_, B_, O_>, dim3(blocks), dim3(256), 0, s, p);
   QNN_ADD(false, false, false) QNN_ADD(false, false, true) QNN_ADD(false, true, false) QNN_ADD(false, true, true)
   QNN_ADD(true, false, false) QNN_ADD(true, false, true) QNN_ADD(true, true, false) QNN_ADD(true, true, true)
 #undef QNN_ADD
@@ -92,6 +94,8 @@ cudaError_t launch_add(const AddParams& p, cudaStream_t s) {
 // VEC channels per thread (16: one uint4 per tap, C % 16 == 0 and aligned pitches; else 1).
 template <int VEC, bool S8, bool AVG>
 __global__ void __launch_bounds__(256) pool_kernel(const __grid_constant__ PoolParams p) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const int G = p.C / VEC;
   const long long total = (long long)p.N * p.P * p.Q * G;
   const uint8_t* in = reinterpret_cast<const uint8_t*>(p.in);
@@ -171,6 +175,8 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t m) {
 template <bool S8, bool AVG, int TQ>
 __global__ void __launch_bounds__(256) pool16_kernel(const __grid_constant__ PoolParams p, FastDiv fdG,
                                                       FastDiv fdQB, FastDiv fdP) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger: the
+                   // next kernel's CTAs would take this multi-wave grid's slots while waiting)
   const int G = p.C >> 4;
   const int QB = (p.Q + TQ - 1) / TQ;
   const uint32_t total = (uint32_t)p.N * p.P * QB * G;
@@ -278,7 +284,7 @@ cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
     const FastDiv fdG = make_fastdiv((uint32_t)(p.C / 16)), fdQB = make_fastdiv((uint32_t)((p.Q + kTQ - 1) / kTQ)),
                   fdP = make_fastdiv((uint32_t)p.P);
 #define QNN_POOL16(S_, A_) \
-  if (p.s8 == S_ && p.avg == A_) pool16_kernel<S_, A_, kTQ><<<blocks, 256, 0, s>>>(p, fdG, fdQB, fdP);
+  if (p.s8 == S_ && p.avg == A_) launch_pdl(pool16_kernel<S_, A_, kTQ>, dim3(blocks), dim3(256), 0, s, p, fdG, fdQB, fdP);
     QNN_POOL16(false, false) QNN_POOL16(false, true) QNN_POOL16(true, false) QNN_POOL16(true, true)
 #undef QNN_POOL16
     count_launch();
@@ -287,7 +293,7 @@ cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
   const long long total = (long long)p.N * p.P * p.Q * (v16 ? p.C / 16 : p.C);
   const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)sms * 16));
 #define QNN_POOL(V_, S_, A_) \
-  if ((v16 ? 16 : 1) == V_ && p.s8 == S_ && p.avg == A_) pool_kernel<V_, S_, A_><<<blocks, 256, 0, s>>>(p);
+  if ((v16 ? 16 : 1) == V_ && p.s8 == S_ && p.avg == A_) launch_pdl(pool_kernel<V_, S_, A_>, dim3(blocks), dim3(256), 0, s, p);
   QNN_POOL(16, false, false) QNN_POOL(16, false, true) QNN_POOL(16, true, false) QNN_POOL(16, true, true)
   QNN_POOL(1, false, false) QNN_POOL(1, false, true) QNN_POOL(1, true, false) QNN_POOL(1, true, true)
 #undef QNN_POOL

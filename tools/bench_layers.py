@@ -45,9 +45,13 @@ class Timer:
     every rep by READING a 512 MB buffer (a write-based flush would leave ~126 MB
     of dirty lines whose write-back lands inside the timed op)."""
 
-    def __init__(self, flush_mb=512):
+    def __init__(self, flush_mb=512, flush=True, b2b=1):
         self.flush = torch.ones(flush_mb * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
         self.sink = torch.empty((), dtype=torch.float32, device="cuda")
+        # flush=False, b2b=k: the graph holds k back-to-back copies of the op and the time is per
+        # copy -- the steady-state cost of a launch whose inputs / code may still be in L2 (the
+        # per-launch floor of small layers: compare with the flushed single replay)
+        self.do_flush, self.b2b = flush, b2b
 
     def time(self, fn, reps=10, warmup=3):
         s = torch.cuda.Stream()
@@ -59,16 +63,18 @@ class Timer:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn()
+            for _ in range(self.b2b):
+                fn()
         ts = []
         for _ in range(reps):
-            torch.sum(self.flush, dim=0, out=self.sink)
+            if self.do_flush:
+                torch.sum(self.flush, dim=0, out=self.sink)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             g.replay()
             b.record()
             b.synchronize()
-            ts.append(a.elapsed_time(b))
+            ts.append(a.elapsed_time(b) / self.b2b)
         # event timestamps tick in ~2 us steps here: a trimmed mean over many reps averages the
         # quantisation out where a median would keep it
         ts.sort()
@@ -100,9 +106,10 @@ def main():
     ap.add_argument("--reps", type=int, default=40)
     ap.add_argument("--per-tensor", action="store_true", help="u8 weights with zp_W != 0 (TFLite style)")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--b2b", type=int, default=0, help="no L2 flush; time K back-to-back launches per replay")
     args = ap.parse_args()
     hbm, tc = peaks()
-    t = Timer()
+    t = Timer(flush=args.b2b == 0, b2b=max(1, args.b2b))
     rows = []
 
     def report(name, ms, macs=0, bytes_=0):
