@@ -690,11 +690,11 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     std::fprintf(stderr,
                  "[qnn plan] N%d C%d %dx%d K%d %dx%d s%d: BK%d BN%d num_m%d num_n%d chunks%d stages%d kps%d b_res%d "
                  "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB) trans%d t_build%d "
-                 "wsplit%d\n",
+                 "wsplit%d (t: stages%d wres%d bufs%d Kt%d)\n",
                  d->N, d->C, d->H, d->W, d->K, d->R, d->S, d->stride_h, pl.BK, pl.BN, pl.num_m, pl.num_n,
                  pl.nchunks, pl.stages, pl.kps, pl.b_res_kb, (int)pl.im2col, (int)pl.fold, (int)pl.pad_copy,
                  (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes, (int)pl.trans,
-                 (int)pl.t_build, (int)pl.wsplit);
+                 (int)pl.t_build, (int)pl.wsplit, pl.t_stages, (int)pl.t_wres, pl.t_bufs, pl.t_Kt);
   return QNN_OK;
 }
 
