@@ -581,11 +581,12 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
   }
   {
     // wide pointwise layers: the channel-major GEMM keeps each output channel's requantize
-    // constants in registers.  QNN_NO_TRANS=1 keeps the pixel-major kernel (A/B measurements);
-    // K_out = 64 runs as half a 128-channel block only with QNN_TRANS_MINK=64 (measured no
-    // faster than the pixel-major kernel on ResNet-50 layer1)
+    // constants in registers.  QNN_NO_TRANS=1 keeps the pixel-major kernel (A/B measurements).
+    // K_out = 64 runs as half a 128-channel block: since the 16x256b epilogue, faster than the
+    // pixel-major kernel (ResNet-50 b256 layer1 conv1 44 -> 34 us); QNN_TRANS_MINK=128 keeps
+    // those layers pixel-major
     static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
-    static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 128;
+    static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 64;
     if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows && d->groups == 1 &&
         (!pl.any_zpw || pl.wsplit) && (d->kernel_dtype == QNN_S8 || pl.wsplit) && pl.requant &&
         (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&

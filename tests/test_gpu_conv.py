@@ -475,8 +475,10 @@ def test_wide_pointwise_channel_major(cfg):
     assert np.array_equal(got, want), mismatch_report(got, want)
 
 
-def test_pointwise_k64_channel_major_subprocess():
-    """QNN_TRANS_MINK=64: K_out = 64 on the channel-major kernel (half a channel block)."""
+@pytest.mark.parametrize("mink", ["64", "128"], ids=["channel_major", "pixel_major"])
+def test_pointwise_k64_channel_major_subprocess(mink):
+    """K_out = 64 pointwise: on the channel-major kernel as half a channel block (the default,
+    QNN_TRANS_MINK=64) and on the pixel-major kernel (QNN_TRANS_MINK=128)."""
     import os
     import subprocess
     import sys
@@ -492,7 +494,7 @@ for i, (C, adt, mode) in enumerate([(256, "u8", "upward"), (64, "s8", "tonearest
 print("OK")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_TRANS_MINK="64"),
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_TRANS_MINK=mink),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
 
