@@ -1016,6 +1016,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
         }
         tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights (or split parts), B = activations
         tp.wsplit = pl.wsplit;
+        static const bool one_set = std::getenv("QNN_TEPI_ONESET") != nullptr;   // (A/B measurements)
+        tp.esets = (pl.t_build || one_set) ? 1 : 2;
         tp.mult = reinterpret_cast<const int32_t*>(pk + pl.pk_mult);
         tp.rsh = reinterpret_cast<const int32_t*>(pk + pl.pk_rsh);
         tp.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);

@@ -232,6 +232,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
   // epilogue warps: the quads holding live channels (all 4, or K_out / 32 in build mode, whose
   // quads 2 and 3 build the X' tiles)
   const int ep_quads = build ? (p.Kout + 31) / 32 : 4;
+  // two epilogue sets on alternate tiles: while one set waits on its TMEM loads or barriers the
+  // other computes (one set of 16 warps on each tile leaves every SMSP idle at the same points)
+  const bool sets2 = !RES && !build && p.esets == 2;
   __shared__ __align__(8) uint64_t full[8], empty[8], tfull[kTNacc], tempty[kTNacc], wfull, rbar[8], rawfull[8],
       rawempty[8];
   __shared__ uint32_t tmem_slot;
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     for (int a = 0; a < kTNacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * ep_quads);   // 4 column groups x live quads
+      mbar_init(&tempty[a], (sets2 ? 2 : 4) * ep_quads);   // the tile's column groups x live quads
     }
     mbar_init(&wfull, 1);
     for (int g = 0; g < 8; ++g) mbar_init(&rbar[g], 1);   // per (group, staging buffer)
@@ -525,8 +528,54 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const uint32_t sw1 = out_rb == 128 ? (uint32_t)(2 * u + 1) : sw0;
     const uint32_t st_off0 = (uint32_t)(2 * u) * out_rb + ((ch16 ^ sw0) << 4) + (uint32_t)((j & 3) << 2);
     const uint32_t st_off1 = (uint32_t)(2 * u + 1) * out_rb + ((ch16 ^ sw1) << 4) + (uint32_t)((j & 3) << 2);
+    if (sets2) {
+      // set = grp / 2 takes the tiles it = set (mod 2), i.e. accumulator `set`; its two column
+      // groups cover 128 pixels each, as two 64-pixel chunks (staging buffer c when there are two)
+      const int set = grp >> 1, sg = grp & 1;
+      int it = set;
+      for (int pt = px_first + set * px_step; pt < npt; pt += 2 * px_step, it += 2) {
+        const int acc = set;
+        QNN_TEPI_WAIT(&tfull[acc], (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const int colrel = sg * (2 * kTCols) + c * kTCols;
+          uint8_t* const stage_out = gstage + (nbufs == 2 ? c * gbytes : 0);
+          const uint32_t sbase = smem_u32(stage_out);
+          if (gleader) bulk_wait_read_dyn(nbufs - 1);   // the store that last used this buffer has read it
+          named_bar_sync(1 + grp, 32 * ep_quads);
+          const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)colrel;
+          uint32_t va0[16], vb0[16], va1[16], vb1[16];
+          tmem_ld_16x256b_x4(tb, va0);
+          tmem_ld_16x256b_x4(tb + (16u << 16), vb0);
+          tmem_ld_16x256b_x4(tb + 32, va1);
+          tmem_ld_16x256b_x4(tb + 32 + (16u << 16), vb1);
+          tmem_wait16x2(va0, vb0);
+          tmem_wait16x2(va1, vb1);
+          tc_fence_before();
+          __syncwarp();
+          if (c == 1 && lane == 0) mbar_arrive(&tempty[acc]);   // this warp is done with the accumulator
+          if (!quad_live) {
+          } else if (all_fast) {
+            t_epilogue<MODE, true, CLAMP, S8OUT, false>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
+            t_epilogue<MODE, true, CLAMP, S8OUT, false>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
+                                                        sbase + 32 * out_rb + st_off1, out_rb);
+          } else {
+            t_epilogue<MODE, false, CLAMP, S8OUT, false>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
+            t_epilogue<MODE, false, CLAMP, S8OUT, false>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
+                                                         sbase + 32 * out_rb + st_off1, out_rb);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1 + grp, 32 * ep_quads);
+          if (gleader) {
+            tma_store_2d(&tmC, stage_out, ch * kTBM, pt * kTBN + colrel);
+            bulk_commit();
+          }
+        }
+      }
+    }
     int it = 0;
-    for (int pt = px_first; pt < npt; pt += px_step, ++it) {
+    for (int pt = sets2 ? npt : px_first; pt < npt; pt += px_step, ++it) {
       const int acc = it % kTNacc;
       uint8_t* const stage_out = gstage + (nbufs == 2 ? (it & 1) * gbytes : 0);
       const uint32_t sbase = smem_u32(stage_out);

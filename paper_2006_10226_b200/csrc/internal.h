@@ -81,6 +81,8 @@ struct GemmTParams {
   int32_t zp_out, lo, hi;
   int stage_bufs;         // output staging buffers per column group (1 or 2)
   int wsplit;             // weights packed as W - zp_W[k] in two s8 parts: two A k-blocks per k-block
+  int esets;              // 2: two epilogue sets of 8 warps take alternate tiles (no residual, not
+                          // build mode), each warp 2 x 64 pixel columns; else all 16 warps per tile
   int out_rb;             // staging / TMA-store row bytes: 128 (min(K_out, 128) in build mode)
   // build mode (small-C stems, K_out <= 64): the B operand X'[pixel][s*C + c] (one 32-byte
   // k-block per filter row, width fold of P:259's zero-point-padded input) is built in shared
