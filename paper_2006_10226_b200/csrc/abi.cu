@@ -215,6 +215,7 @@ struct ConvPlan {
   size_t pk_zpv = 0;
   bool trans = false, t_wres = false;
   int t_stages = 0, t_Kt = 0, t_bufs = 1;
+  bool t_pair = false;   // CTA pairs (cta_group::2) over channel-block pairs: M = 256 per MMA
   // channel-major build mode (small-C stems with K_out <= 64): X' built in smem by the idle quads
   bool t_build = false;
   int t_ib = 0, t_nr = 0, t_slot = 0, t_raw = 0, t_rstages = 0;
@@ -592,20 +593,38 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
         (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
         pl.out_cs % 16 == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
       const int num_kb = pl.nchunks;   // one tap
+      // CTA pairs (cta_group::2, each CTA staging half of every pixel tile: operand bytes per SM
+      // per MAC drop by 1.5x) where a single CTA would stream its weights and K_out >= 512 --
+      // the layers bound by what an SM can take in (ResNet-50 layer4 conv1: -5..11%).  On
+      // resident-weight and K_out = 256 layers the pair measured slower (the two CTAs' epilogues
+      // and pipelines run in lockstep: conv3 +20-30%).  QNN_PAIR=0 / 1 forces it off / on where
+      // the channel blocks pair up.
+      static const int pair_env = std::getenv("QNN_PAIR") ? std::atoi(std::getenv("QNN_PAIR")) : -1;
+      const bool can_pair = (round_up(d->K, 128) / 128) % 2 == 0;
+      bool pair = false;
+      if (can_pair && pair_env != 0) {
+        if (pair_env == 1) {
+          pair = true;
+        } else if (d->K >= 512) {   // would a single CTA stream its weights?
+          const int st_res = gemm_t_max_stages(pl.BK, num_kb, true, 1, -1, 0, 128, bparts);
+          pair = !(st_res >= 3 && gemm_t_smem_bytes(pl.BK, num_kb, st_res, true, 1, -1, 0, 128, bparts) <= 226 * 1024);
+        }
+      }
       // preference: resident weights with a second output staging buffer per column group
       // (>= 4 stages), then resident weights with one, then streamed weights
       const int opts[3][2] = {{2, 1}, {1, 1}, {1, 0}};   // {buffers, weights resident}
       for (const auto& o : opts) {
         const int bufs = o[0];
         const bool w_res = o[1] != 0;
-        const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res, bufs, -1, 0, 128, bparts);
+        const int stages = gemm_t_max_stages(pl.BK, num_kb, w_res, bufs, -1, 0, 128, bparts, pair);
         if (stages >= (bufs == 2 ? 4 : 3) &&
-            gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res, bufs, -1, 0, 128, bparts) <= 226 * 1024) {
+            gemm_t_smem_bytes(pl.BK, num_kb, stages, w_res, bufs, -1, 0, 128, bparts, pair) <= 226 * 1024) {
           pl.trans = true;
           pl.t_wres = w_res;
           pl.t_stages = stages;
           pl.t_bufs = bufs;
           pl.t_Kt = round_up(d->K, 128);
+          pl.t_pair = pair;
           break;
         }
       }
@@ -691,11 +710,11 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     std::fprintf(stderr,
                  "[qnn plan] N%d C%d %dx%d K%d %dx%d s%d: BK%d BN%d num_m%d num_n%d chunks%d stages%d kps%d b_res%d "
                  "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB) trans%d t_build%d "
-                 "wsplit%d (t: stages%d wres%d bufs%d Kt%d)\n",
+                 "wsplit%d (t: stages%d wres%d bufs%d Kt%d pair%d)\n",
                  d->N, d->C, d->H, d->W, d->K, d->R, d->S, d->stride_h, pl.BK, pl.BN, pl.num_m, pl.num_n,
                  pl.nchunks, pl.stages, pl.kps, pl.b_res_kb, (int)pl.im2col, (int)pl.fold, (int)pl.pad_copy,
                  (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes, (int)pl.trans,
-                 (int)pl.t_build, (int)pl.wsplit, pl.t_stages, (int)pl.t_wres, pl.t_bufs, pl.t_Kt);
+                 (int)pl.t_build, (int)pl.wsplit, pl.t_stages, (int)pl.t_wres, pl.t_bufs, pl.t_Kt, (int)pl.t_pair);
   return QNN_OK;
 }
 
@@ -972,7 +991,8 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
         small_tensor_fixup(&tmX, rowlen * d->H * d->N);
       } else {
-        okx = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK, kGemmTBN);
+        okx = encode_2d(&tmX, A, (uint64_t)a_chan, (uint64_t)pl.M, (uint64_t)a_pitch, pl.BK,
+                        pl.t_pair ? kGemmTBN / 2 : kGemmTBN);   // (pair: each CTA loads half a tile)
       }
       bool okt = okx &&
                  encode_2d(&tmW, pk + pl.pk_wt, (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), (uint64_t)pl.t_Kt,
@@ -1014,7 +1034,9 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
           tp.fdQ = make_fastdiv((uint32_t)pl.Q);
           tp.fdP = make_fastdiv((uint32_t)pl.P);
         }
-        tp.idesc = make_idesc_i8(1, a_signed, 128, kGemmTBN);   // A = s8 weights (or split parts), B = activations
+        // A = s8 weights (or split parts), B = activations; a pair's MMA has M = 256
+        tp.idesc = make_idesc_i8(1, a_signed, pl.t_pair && !pl.t_build ? 256 : 128, kGemmTBN);
+        tp.pair = pl.t_pair && !pl.t_build ? 1 : 0;
         tp.wsplit = pl.wsplit;
         static const bool one_set = std::getenv("QNN_TEPI_ONESET") != nullptr;   // (A/B measurements)
         tp.esets = (pl.t_build || one_set) ? 1 : 2;

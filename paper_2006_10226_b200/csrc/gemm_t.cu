@@ -21,6 +21,7 @@
 // tiles advance by grid / blocks.
 // Warps: 0-15 epilogue (warp w: TMEM lanes 32*(w%4), pixel columns 64*(w/4)), 16 TMA
 // producer, 17 MMA issuer + TMEM allocator (2 accumulators x 256 columns).
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -192,25 +193,26 @@ constexpr int kTSmemMax = 227 * 1024 - 1024;   // dynamic budget (the barriers a
 // carries its weight k-block next to the activation k-block.  build_raw_bytes >= 0: build mode,
 // a stage holds all num_kb X' k-blocks of a tile plus its raw input rows (weights resident)
 size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes,
-                         int rstages, int out_rb, int wparts) {
-  // (wparts = 2: split weights, two weight k-blocks per activation k-block)
+                         int rstages, int out_rb, int wparts, bool pair) {
+  // (wparts = 2: split weights, two weight k-blocks per activation k-block; pair: a CTA of a
+  // cta_group::2 pair stages half of each pixel tile)
   const size_t stage = build_raw_bytes >= 0 ? (size_t)num_kb * kTBN * BK
-                                            : (size_t)kTBN * BK + (w_res ? 0 : (size_t)kTBM * BK * wparts);
+                                            : (size_t)(pair ? kTBN / 2 : kTBN) * BK + (w_res ? 0 : (size_t)kTBM * BK * wparts);
   const size_t raw = build_raw_bytes >= 0 ? (size_t)rstages * build_raw_bytes : 0;
   return 1024 + (size_t)stages * stage + (w_res ? (size_t)num_kb * kTBM * BK * wparts : 0) + raw +
          (size_t)4 * kTCols * out_rb * stage_bufs + 256;
 }
 
 int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes, int rstages, int out_rb,
-                      int wparts) {
+                      int wparts, bool pair) {
   int s = 8;
-  while (s > 1 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs, build_raw_bytes, rstages, out_rb, wparts) >
+  while (s > 1 && gemm_t_smem_bytes(BK, num_kb, s, w_res, stage_bufs, build_raw_bytes, rstages, out_rb, wparts, pair) >
                       (size_t)kTSmemMax)
     --s;
   return s;
 }
 
-template <int MODE, bool CLAMP, bool S8OUT, bool RES>
+template <int MODE, bool CLAMP, bool S8OUT, bool RES, bool PAIR>
 __global__ void __launch_bounds__(kTThreads, 1)
     qnn_gemm_t_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
@@ -218,9 +220,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int BK = p.BK, stages = p.stages, num_kb = p.num_kb;
-  const uint32_t x_bytes = (uint32_t)kTBN * BK, w_bytes = (uint32_t)kTBM * BK;
-  const bool w_res = p.w_res;
   const bool build = p.build;
+  // CTA pair (cta_group::2): the pair's two channel blocks form one M = 256 MMA; each CTA stages
+  // half of every pixel tile (rows 128 r, +128) and its own weights; the leader (rank 0) issues
+  // the MMAs; the TMA loads of both CTAs complete on the leader's barriers; the commits reach
+  // both CTAs' barriers; every epilogue warp frees the accumulator on the leader's barrier
+  // (a template parameter: kernels with cta_group::2 instructions must be launched as clusters)
+  const bool pair = PAIR && !build;
+  const uint32_t prank = pair ? cluster_rank() : 0u;
+  const uint32_t x_bytes = (uint32_t)(pair ? kTBN / 2 : kTBN) * BK, w_bytes = (uint32_t)kTBM * BK;
+  const bool w_res = p.w_res;
   const int wparts = p.wsplit ? 2 : 1;   // split weights (zp_W folded): two weight k-blocks per k-block
   // X: stages x [256 pixels][BK] (build mode: stages x num_kb x [256 pixels][32], built in smem)
   const size_t x_stage = build ? (size_t)num_kb * x_bytes : (size_t)x_bytes;
@@ -260,27 +269,42 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     for (int a = 0; a < kTNacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], (sets2 ? 2 : 4) * ep_quads);   // the tile's column groups x live quads
+      // the tile's column groups x live quads (pair: the leader counts both CTAs' warps)
+      mbar_init(&tempty[a], (sets2 ? 2 : 4) * ep_quads * (pair ? 2 : 1));
     }
     mbar_init(&wfull, 1);
     for (int g = 0; g < 8; ++g) mbar_init(&rbar[g], 1);   // per (group, staging buffer)
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc(&tmem_slot, 512);
+  if (warp == kMmaWarp) {
+    if (pair)
+      tmem_alloc2(&tmem_slot, 512);
+    else
+      tmem_alloc(&tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
+  if (pair) cluster_sync_all();   // both CTAs' barriers initialised before any cross-CTA signal
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+  // pair: the leader's barriers as cluster addresses (TMA completions, accumulator releases)
+  const uint32_t full_l = pair ? cluster_addr(&full[0], 0) : 0u, wfull_l = pair ? cluster_addr(&wfull, 0) : 0u,
+                 tempty_l = pair ? cluster_addr(&tempty[0], 0) : 0u;
   pdl_trigger();                        // the next layer's kernel may launch and run its prologue
   if (warp != kProdWarp) pdl_wait();    // (the producer waits after issuing the resident weights)
 
   if (warp == kProdWarp) {
     const bool leader = elect_one();
     if (leader && w_res && px_first < npt) {
-      // (split weights: part a's num_kb k-blocks, then part b's)
-      mbar_arrive_expect_tx(&wfull, (uint32_t)(num_kb * wparts) * w_bytes);
-      for (int kb = 0; kb < num_kb * wparts; ++kb)
-        tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
+      // (split weights: part a's num_kb k-blocks, then part b's; pair: both CTAs' weights on the
+      // leader's barrier)
+      if (prank == 0) mbar_arrive_expect_tx(&wfull, (uint32_t)(num_kb * wparts) * w_bytes * (pair ? 2u : 1u));
+      for (int kb = 0; kb < num_kb * wparts; ++kb) {
+        if (pair)
+          tma_load_2d_pair(sW + (size_t)kb * w_bytes, &tmW, wfull_l, kb * BK, ch * kTBM);
+        else
+          tma_load_2d(sW + (size_t)kb * w_bytes, &tmW, &wfull, kb * BK, ch * kTBM);
+      }
     }
     pdl_wait();   // activations are the previous kernel's output
     int stage = 0;
@@ -314,7 +338,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         QNN_T_WAIT(&empty[stage], phase ^ 1);
         if (leader && kb == 0) t_trace(p.trace, 0, (pt - px_first) / px_step);
-        if (leader) {
+        if (leader && pair) {
+          const uint32_t fb = full_l + (uint32_t)stage * 8u;
+          if (prank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (x_bytes + (w_res ? 0 : w_bytes * wparts)));
+          tma_load_2d_pair(sX + (size_t)stage * x_bytes, &tmX, fb, kb * BK, pt * kTBN + (int)prank * (kTBN / 2));
+          if (!w_res) {
+            tma_load_2d_pair(sW + (size_t)stage * w_bytes * wparts, &tmW, fb, kb * BK, ch * kTBM);
+            if (wparts == 2)
+              tma_load_2d_pair(sW + (size_t)stage * w_bytes * 2 + w_bytes, &tmW, fb, (num_kb + kb) * BK, ch * kTBM);
+          }
+        } else if (leader) {
           mbar_arrive_expect_tx(&full[stage], x_bytes + (w_res ? 0 : w_bytes * wparts));
           tma_load_2d(sX + (size_t)stage * x_bytes, &tmX, &full[stage], kb * BK, pt * kTBN);
           if (!w_res) {
@@ -331,7 +364,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp && prank == 0) {   // (pair: the peer's MMA warp only allocates TMEM)
     const bool leader = elect_one();
     const uint64_t wdesc0 = make_sdesc(smem_u32(sW), BK), xdesc0 = make_sdesc(smem_u32(sX), BK);
     const uint32_t idesc = p.idesc, w16 = w_bytes >> 4, x16 = x_bytes >> 4;
@@ -377,12 +410,20 @@ __global__ void __launch_bounds__(kTThreads, 1)
                          xd = xdesc0 + (uint64_t)((stage * x_stage) >> 4);
           // split weights: part b resident num_kb blocks on, or right after part a in the stage
           const uint64_t wsplit16 = wparts == 2 ? (uint64_t)(w_res ? num_kb : 1) * w16 : 0;
-          if (!(kTInstrument && (p.dbg & 8)))   // (instrumented builds: 8 skips the MMAs)
+          if (pair) {
             for (int k = 0; k < ksteps; ++k) {
-              umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
-              if (wparts == 2) umma_i8(d, wd + wsplit16 + 2 * k, xd + 2 * k, idesc, 1u);
+              umma_i8_pair(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+              if (wparts == 2) umma_i8_pair(d, wd + wsplit16 + 2 * k, xd + 2 * k, idesc, 1u);
             }
-          umma_commit(&empty[stage]);
+            umma_commit_pair(&empty[stage]);   // both CTAs' producers may refill the stage
+          } else {
+            if (!(kTInstrument && (p.dbg & 8)))   // (instrumented builds: 8 skips the MMAs)
+              for (int k = 0; k < ksteps; ++k) {
+                umma_i8(d, wd + 2 * k, xd + 2 * k, idesc, (kb | k) != 0);
+                if (wparts == 2) umma_i8(d, wd + wsplit16 + 2 * k, xd + 2 * k, idesc, 1u);
+              }
+            umma_commit(&empty[stage]);
+          }
         }
         __syncwarp();
         if (++stage == stages) {
@@ -391,7 +432,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
       }
       if (leader) {
-        umma_commit(&tfull[acc]);
+        if (pair)
+          umma_commit_pair(&tfull[acc]);   // both CTAs' epilogues
+        else
+          umma_commit(&tfull[acc]);
         t_trace(p.trace, 256, it);
       }
       __syncwarp();
@@ -554,7 +598,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
           tmem_wait16x2(va1, vb1);
           tc_fence_before();
           __syncwarp();
-          if (c == 1 && lane == 0) mbar_arrive(&tempty[acc]);   // this warp is done with the accumulator
+          if (c == 1 && lane == 0) {   // this warp is done with the accumulator
+            if (pair)
+              mbar_arrive_cluster(tempty_l + (uint32_t)acc * 8u);
+            else
+              mbar_arrive(&tempty[acc]);
+          }
           if (!quad_live) {
           } else if (all_fast) {
             t_epilogue<MODE, true, CLAMP, S8OUT, false>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
@@ -624,7 +673,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (pair)
+          mbar_arrive_cluster(tempty_l + (uint32_t)acc * 8u);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       // (warp-uniform choice: a per-lane branch would be if-converted and issue both paths)
       if ((dbg & 1) || !quad_live) {
       } else if (all_fast && RES && q.rt > 0) {   // (q.rt is uniform: one per-tensor residual multiplier)
@@ -653,9 +707,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  // (pair: the peer's last TMA completions, commits and releases target this CTA's barriers and
+  // TMEM is allocated for the pair, so both CTAs leave together)
+  if (pair) cluster_sync_all();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (pair)
+      tmem_dealloc2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 
@@ -663,31 +723,50 @@ cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream) {
   const bool res = p.has_res;
+  const bool pair = p.pair != 0 && !p.build;
   const size_t smem = gemm_t_smem_bytes(p.BK, p.num_kb, p.stages, p.w_res, p.stage_bufs,
-                                       p.build ? p.b_raw_bytes : -1, p.rstages, p.out_rb, p.wsplit ? 2 : 1);
+                                       p.build ? p.b_raw_bytes : -1, p.rstages, p.out_rb, p.wsplit ? 2 : 1, pair);
   if (smem > (size_t)kTSmemMax || p.stages > 8) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-#define QNN_GT(M_, C_, S_, R_)                                                                             \
-  if (mode == M_ && clamp == C_ && s8out == S_ && res == R_) {                                             \
-    auto kern = qnn_gemm_t_kernel<M_, C_, S_, R_>;                                                         \
+#define QNN_GT(M_, C_, S_, R_, P_)                                                                         \
+  if (mode == M_ && clamp == C_ && s8out == S_ && res == R_ && pair == P_) {                               \
+    auto kern = qnn_gemm_t_kernel<M_, C_, S_, R_, P_>;                                                     \
     static int attr_done[64] = {0};   /* per device: a process may drive several GPUs */                  \
     if (dev >= 64 || !attr_done[dev]) {                                                                    \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmemMax);  \
       if (e != cudaSuccess) return e;                                                                      \
       if (dev < 64) attr_done[dev] = 1;                                                                    \
     }                                                                                                      \
-    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kTThreads), smem, stream, tmX, tmW, tmC, tmR, p);    \
+    int g = grid;                                                                                          \
+    if (pair) {   /* as many CTAs as pairs can be co-resident (GPCs with odd SM counts) */                  \
+      static int maxc[64] = {0};                                                                           \
+      static size_t maxc_smem[64] = {0};                                                                   \
+      int m = 0;                                                                                           \
+      if (dev < 64 && maxc_smem[dev] == smem) {                                                            \
+        m = maxc[dev];                                                                                     \
+      } else {                                                                                             \
+        m = max_active_clusters(kern, dim3(kTThreads), smem, 2);                                           \
+        if (dev < 64) { maxc[dev] = m; maxc_smem[dev] = smem; }                                            \
+      }                                                                                                    \
+      g = std::min(g, 2 * m);                                                                              \
+      g -= g % p.num_ch_tiles;                                                                             \
+      if (g <= 0) return cudaErrorInvalidValue;                                                            \
+    }                                                                                                      \
+    cudaError_t e = launch_ex(kern, dim3(g), dim3(kTThreads), smem, stream, pair ? 2 : 1, tmX, tmW, tmC,     \
+                              tmR, p);                                                                     \
     count_launch();                                                                                        \
     if (e == cudaSuccess) e = cudaGetLastError();                                                          \
     if (e != cudaSuccess && std::getenv("QNN_PLAN_TRACE"))                                                 \
       std::fprintf(stderr, "[qnn gemm_t] launch failed: %s\n", cudaGetErrorString(e));                    \
     return e;                                                                                              \
   }
-#define QNN_GT_R(M_, C_, S_) QNN_GT(M_, C_, S_, false) QNN_GT(M_, C_, S_, true)
+#define QNN_GT_P(M_, C_, S_, R_) QNN_GT(M_, C_, S_, R_, false) QNN_GT(M_, C_, S_, R_, true)
+#define QNN_GT_R(M_, C_, S_) QNN_GT_P(M_, C_, S_, false) QNN_GT_P(M_, C_, S_, true)
   QNN_GT_R(0, false, false) QNN_GT_R(0, false, true) QNN_GT_R(0, true, false) QNN_GT_R(0, true, true)
   QNN_GT_R(1, false, false) QNN_GT_R(1, false, true) QNN_GT_R(1, true, false) QNN_GT_R(1, true, true)
 #undef QNN_GT_R
+#undef QNN_GT_P
 #undef QNN_GT
   return cudaErrorInvalidValue;
 }

@@ -81,6 +81,8 @@ struct GemmTParams {
   int32_t zp_out, lo, hi;
   int stage_bufs;         // output staging buffers per column group (1 or 2)
   int wsplit;             // weights packed as W - zp_W[k] in two s8 parts: two A k-blocks per k-block
+  int pair;               // CTA pairs (clusters of 2, cta_group::2): MMA M = 256 over the two channel
+                          // blocks of a pair, each CTA staging half of every pixel tile
   int esets;              // 2: two epilogue sets of 8 warps take alternate tiles (no residual, not
                           // build mode), each warp 2 x 64 pixel columns; else all 16 warps per tile
   int out_rb;             // staging / TMA-store row bytes: 128 (min(K_out, 128) in build mode)
@@ -97,9 +99,9 @@ struct GemmTParams {
   unsigned long long* trace;   // QNN_GEMM_TRACE (instrumented builds only): CTA 0 clock64 events
 };
 size_t gemm_t_smem_bytes(int BK, int num_kb, int stages, bool w_res, int stage_bufs, int build_raw_bytes = -1,
-                         int rstages = 0, int out_rb = 128, int wparts = 1);
+                         int rstages = 0, int out_rb = 128, int wparts = 1, bool pair = false);
 int gemm_t_max_stages(int BK, int num_kb, bool w_res, int stage_bufs, int build_raw_bytes = -1, int rstages = 0,
-                      int out_rb = 128, int wparts = 1);
+                      int out_rb = 128, int wparts = 1, bool pair = false);
 cudaError_t launch_gemm_t(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmC,
                           const CUtensorMap& tmR, const GemmTParams& p, int mode, bool clamp, bool s8out, int grid,
                           cudaStream_t stream);
@@ -151,19 +153,55 @@ struct GemmParams {
 // tail; the kernel must call pdl_wait() before it reads or writes activations.  QNN_NO_PDL=1
 // launches normally (A/B measurements).
 bool pdl_enabled();
+// cluster > 1: thread-block clusters of that many CTAs along x
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                      Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = (unsigned)cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n++].val.clusterDim.z = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  return launch_ex(kern, grid, block, smem, s, 1, static_cast<Args&&>(args)...);
+}
+// co-resident clusters of `cluster` CTAs of `kern` with `smem` dynamic bytes (0 on error)
+template <typename... KArgs>
+int max_active_clusters(void (*kern)(KArgs...), dim3 block, size_t smem, int cluster) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * 64);
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 constexpr int kGemmBM = 128;
