@@ -574,3 +574,36 @@ def test_legalize_u8_weights_to_s8(cfg):
         ys.append(op(x).cpu().numpy())
     assert np.array_equal(ys[0], want), mismatch_report(ys[0], want)
     assert np.array_equal(ys[1], want), mismatch_report(ys[1], want)
+
+
+def test_channel_major_cta_pair_subprocess():
+    """QNN_PAIR=1: every channel-major layer whose channel blocks pair up runs as CTA pairs
+    (cta_group::2, M = 256 over two SMs): plain, split-weight (zp_W vector) and streamed-weight
+    shapes, ragged pixel tails, bit-exact against the oracle.  (By default only streamed-weight
+    layers with K_out >= 512 pair up; the ResNet-50 layer4 conv1 shapes at batch 2 are one.)"""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from gpu_helpers import gpu_conv, oracle_conv
+from workloads import gen
+cases = [(2, 64, 9, 7, 256, "upward"), (1, 256, 13, 11, 512, "tonearest"), (2, 2048, 7, 7, 512, "upward"),
+         (1, 1024, 5, 9, 1024, "upward")]
+for i, (N, C, H, W, K, mode) in enumerate(cases):
+    case = gen.conv_case(1850 + i, N, C, H, W, K, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), 1, "u8", "s8", rounding=mode)
+    _, _, y = gpu_conv(case)
+    assert np.array_equal(y.cpu().numpy(), oracle_conv(case)), i
+case = gen.conv_case(1860, 2, 128, 9, 9, 256, 1, 1, (1, 1), (0, 0, 0, 0), (1, 1), 1, "u8", "s8", relu=False)
+g = np.random.default_rng(1861)
+case.zp_W = g.integers(-127, 128, size=256).astype(np.int32)
+case.s_out = float(np.float32(case.s_out * 2))
+_, _, y = gpu_conv(case)
+assert np.array_equal(y.cpu().numpy(), oracle_conv(case)), "split"
+print("OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_PAIR="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
