@@ -190,6 +190,7 @@ struct ConvPlan {
   int a_ib = 0, a_nr = 0, a_slot_bytes = 0, a_raw_bytes = 0;
   bool a_zpfill = false;  // a_build writes zp_A outside the image (single border class)
   bool a_rows = false;    // stride-1 convs: staged input rows + per-tap descriptor offsets
+  bool pair = false;      // CTA pairs (cta_group::2): consecutive M tiles form one M = 256 MMA
   int a_Wp = 0, a_T = 0, a_nri = 0, a_stage_bytes = 0;
   int Ct = 0;            // channel count / pitch seen by TMA
   // geometry of the GEMM as the kernel sees it (differs from the descriptor when folded)
@@ -667,6 +668,31 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
       }
     }
   }
+  {
+    // pixel-major CTA pairs (cta_group::2: each CTA of a cluster of 2 stages its own A tile and
+    // half of the B tile, 1.5x fewer operand bytes per SM per MAC): only with QNN_PAIR=1.
+    // Measured on the ResNet-50 b256 streamed-weight layers: layer3 3x3 -4..+3%, layer4 3x3 and
+    // layer3.0.downsample +35% (the pair's two tiles, epilogues and pipelines run in lockstep,
+    // and BN = 192 halves into 96-row B boxes), so the single-CTA plan stays the default.
+    static const int pair_env = std::getenv("QNN_PAIR") ? std::atoi(std::getenv("QNN_PAIR")) : -1;
+    const bool can = pair_env == 1 && !pl.trans && !pl.depthwise && !pl.a_rows && !pl.a_build && !pl.wsplit &&
+                     pl.num_m >= 2 && pl.BN >= 64 && pl.BN % 16 == 0;
+    if (can) {
+      const int ncls = pl.ct.ncr * pl.ct.ncc;
+      const int st = gemm_max_stages(pl.BK, pl.BN, ncls, pl.b_res_kb, pl.kps, pl.a_raw_bytes, pl.a_stage_bytes, 1, true,
+                                     true);
+      if (st >= 3 && gemm_smem_bytes(pl.BK, pl.BN, st, ncls, pl.b_res_kb, pl.kps, pl.a_raw_bytes, pl.a_stage_bytes, 1,
+                                     true, true) <= 227 * 1024) {
+        pl.pair = true;
+        pl.stages = st;
+        // grid in pairs: pair tiles = ceil(num_m / 2) x num_n, a pair keeps one N tile
+        const long long ptiles = (long long)((pl.num_m + 1) / 2) * pl.num_n;
+        const int maxp = sm_count() / 2;
+        pl.grid = 2 * (int)(ptiles <= maxp ? ptiles : (long long)(maxp / pl.num_n) * pl.num_n);
+        if (pl.grid <= 0) pl.pair = false;
+      }
+    }
+  }
   const int taps = d->R * pl.gS;  // GEMM taps (R when folded)
   size_t off = 0;
   pl.pk_w = off;
@@ -710,11 +736,11 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     std::fprintf(stderr,
                  "[qnn plan] N%d C%d %dx%d K%d %dx%d s%d: BK%d BN%d num_m%d num_n%d chunks%d stages%d kps%d b_res%d "
                  "im2col%d fold%d pad_copy%d a_build%d a_rows%d (Wp%d T%d nri%d stage%dB) trans%d t_build%d "
-                 "wsplit%d (t: stages%d wres%d bufs%d Kt%d pair%d)\n",
+                 "wsplit%d ppair%d (t: stages%d wres%d bufs%d Kt%d pair%d)\n",
                  d->N, d->C, d->H, d->W, d->K, d->R, d->S, d->stride_h, pl.BK, pl.BN, pl.num_m, pl.num_n,
                  pl.nchunks, pl.stages, pl.kps, pl.b_res_kb, (int)pl.im2col, (int)pl.fold, (int)pl.pad_copy,
                  (int)pl.a_build, (int)pl.a_rows, pl.a_Wp, pl.a_T, pl.a_nri, pl.a_stage_bytes, (int)pl.trans,
-                 (int)pl.t_build, (int)pl.wsplit, pl.t_stages, (int)pl.t_wres, pl.t_bufs, pl.t_Kt, (int)pl.t_pair);
+                 (int)pl.t_build, (int)pl.wsplit, (int)pl.pair, pl.t_stages, (int)pl.t_wres, pl.t_bufs, pl.t_Kt, (int)pl.t_pair);
   return QNN_OK;
 }
 
@@ -1102,7 +1128,7 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
   if (!ok) return QNN_ERR_UNSUPPORTED;
   ok = encode_2d(&tmB, pk + pl.pk_w, (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), (uint64_t)pl.Kpad,
                  (uint64_t)taps * pl.Cw * (pl.wsplit ? 2 : 1), pl.BK,
-                 pl.BN);
+                 pl.pair ? pl.BN / 2 : pl.BN);
   if (!ok) return QNN_ERR_UNSUPPORTED;
   // 8-bit output through per-warp TMA stores when the output pitch allows it
   // one store box per epilogue column half: 32 rows x (that half's columns), swizzled to match
@@ -1178,8 +1204,10 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
     p.a_raw_bytes = pl.a_raw_bytes;
   }
   // (split weights are s8 parts whatever the kernel dtype)
-  p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8 || pl.wsplit, kGemmBM, pl.BN);
+  p.idesc = make_idesc_i8(d->input_dtype == QNN_S8, d->kernel_dtype == QNN_S8 || pl.wsplit,
+                          pl.pair ? 2 * kGemmBM : kGemmBM, pl.BN);   // (a pair's MMA has M = 256)
   p.wsplit = pl.wsplit;
+  p.pair = pl.pair ? 1 : 0;
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
   ep.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);

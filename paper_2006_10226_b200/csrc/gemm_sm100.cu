@@ -11,20 +11,22 @@ namespace qnn {
 // Each pipeline stage carries kps consecutive k-blocks (one barrier round trip, one
 // commit per stage: amortises the per-stage synchronisation for narrow k-blocks).
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes,
-                       int a_stage_bytes, int bparts, bool out_staging) {
-  // (bparts = 2: split weights, two B k-blocks per A k-block; b_res_kb then counts both parts)
-  const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps, b = (size_t)BN * BK * bparts;
+                       int a_stage_bytes, int bparts, bool out_staging, bool pair) {
+  // (bparts = 2: split weights, two B k-blocks per A k-block; b_res_kb then counts both parts;
+  // pair: a CTA of a cta_group::2 pair stages half of each B k-block)
+  const size_t a = a_stage_bytes ? (size_t)a_stage_bytes : (size_t)kGemmBM * BK * kps,
+               b = (size_t)(pair ? BN / 2 : BN) * BK * bparts;
   const size_t ring = b_res_kb > 0 ? stages * a + (size_t)b_res_kb * (b / bparts) : stages * (a + b * kps);
   return 1024 + ring + (size_t)stages * raw_bytes + (out_staging ? kStageOutBytes : 0) + kParamBytes +
          off_table_bytes(ncls, BN) + 512;
 }
 
 int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes, int a_stage_bytes, int bparts,
-                    bool out_staging) {
+                    bool out_staging, bool pair) {
   const size_t budget = 227 * 1024;
   int s = 8;
   while (s > 2 &&
-         gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes, bparts, out_staging) > budget)
+         gemm_smem_bytes(BK, BN, s, ncls, b_res_kb, kps, raw_bytes, a_stage_bytes, bparts, out_staging, pair) > budget)
     --s;
   return s;
 }
@@ -32,7 +34,8 @@ int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_byt
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC, const GemmParams& p,
                         int mode, bool clamp, int grid, cudaStream_t stream) {
   if (p.wsplit) return launch_gemm_split(tmA, tmB, tmC, p, mode, clamp, grid, stream);
-  return launch_gemm_impl<false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  if (p.pair) return launch_gemm_pair(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  return launch_gemm_impl<false, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
 }
 
 }  // namespace qnn

@@ -29,6 +29,8 @@
 // is done by cvt.pack.sat.  Per-column {M, t} and per-(class, column) K are staged
 // once per N-tile in shared memory and read as broadcast LDS.128 (two columns each).
 #pragma once
+#include <algorithm>
+
 #include "common.cuh"
 #include <cstdio>
 #include <cstdlib>
@@ -86,7 +88,32 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // Taps (r, s) of an R x S grid: A steps `a_col16` per s and `a_row16` per r, B `b_tap16` per
 // tap (the plain k-block sequence is R = 1, S = nk).  The first MMA overwrites the accumulator
 // unless `acc`.
-template <int KS, bool SPLIT>
+// one tcgen05.mma / commit, single CTA or CTA pair (cta_group::2)
+template <bool PAIR>
+__device__ __forceinline__ void umma_x(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (PAIR)
+    umma_i8_pair(d, a, b, idesc, acc);
+  else
+    umma_i8(d, a, b, idesc, acc);
+}
+template <bool PAIR>
+__device__ __forceinline__ void commit_x(uint64_t* bar) {
+  if (PAIR)
+    umma_commit_pair(bar);
+  else
+    umma_commit(bar);
+}
+
+// an epilogue warp hands the accumulator back (PAIR: on the leader's barrier)
+template <bool PAIR>
+__device__ __forceinline__ void release_acc(uint64_t* tempty, int acc, uint32_t tempty_l) {
+  if (PAIR)
+    mbar_arrive_cluster(tempty_l + (uint32_t)acc * 8u);
+  else
+    mbar_arrive(&tempty[acc]);
+}
+
+template <int KS, bool SPLIT, bool PAIR>
 __device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64_t bd, uint32_t idesc, int R, int S,
                                              uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16, uint32_t acc,
                                              uint32_t bsplit16) {
@@ -95,9 +122,9 @@ __device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64
     for (int s = 0; s < S; ++s) {
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
-        umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, k ? 1u : acc);
+        umma_x<PAIR>(d, ad + 2 * k, bd + 2 * k, idesc, k ? 1u : acc);
         // split weights (zp_W folded): the second s8 part of W - zp_W against the same A
-        if (SPLIT) umma_i8(d, ad + 2 * k, bd + bsplit16 + 2 * k, idesc, 1u);
+        if (SPLIT) umma_x<PAIR>(d, ad + 2 * k, bd + bsplit16 + 2 * k, idesc, 1u);
       }
       acc = 1;
       ad += a_col16;
@@ -107,19 +134,19 @@ __device__ __forceinline__ void issue_mma_ks(uint32_t d, uint64_t ad_row, uint64
   }
 }
 
-template <bool SPLIT>
+template <bool SPLIT, bool PAIR>
 __device__ __forceinline__ void issue_mma(int ksteps, uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, int R,
                                           int S, uint32_t a_row16, uint32_t a_col16, uint32_t b_tap16,
                                           uint32_t acc, uint32_t bsplit16) {
   if (ksteps == 4)
-    issue_mma_ks<4, SPLIT>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
+    issue_mma_ks<4, SPLIT, PAIR>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
   else if (ksteps == 2)
-    issue_mma_ks<2, SPLIT>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
+    issue_mma_ks<2, SPLIT, PAIR>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
   else if (ksteps == 1)
-    issue_mma_ks<1, SPLIT>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
+    issue_mma_ks<1, SPLIT, PAIR>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     qnn_gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
@@ -134,7 +161,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // a_build: warps 8..15 build A tiles, warps 0..7 run the epilogue
   const int nepi = p.a_build ? 8 : kGemmEpiWarps;
   const int nsets = gemm_epi_sets(BN, p.num_n_tiles, nepi);
-  const uint32_t a_bytes = kGemmBM * BK, b_bytes = BN * BK;
+  // PAIR (cta_group::2, clusters of 2): the pair's two M tiles form one M = 256 MMA issued by the
+  // leader (rank 0); each CTA stages its own A tile and half of the B tile (BN / 2 rows); TMA
+  // loads of both CTAs complete on the leader's barriers, commits reach both CTAs, every
+  // epilogue warp releases the accumulator on the leader's barrier
+  const uint32_t prank = PAIR ? cluster_rank() : 0u;
+  const uint32_t a_bytes = kGemmBM * BK, b_bytes = (PAIR ? BN / 2 : BN) * BK;
   const bool b_res = p.b_res;
   // SPLIT: weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction), two B
   // k-blocks per A k-block.  A template parameter so the plain kernels carry none of it.
@@ -182,27 +214,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < nacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], nepi / nsets);   // every warp of the set that owns the tile
+      mbar_init(&tempty[a], (nepi / nsets) * (PAIR ? 2 : 1));   // every warp of the set that owns the tile
     }
     mbar_init(bres_full, 1);
     for (int s = 0; s < stages; ++s) mbar_init(&rawfull[s], 1);
     fence_mbar_init();
   }
   if (tracing && threadIdx.x == 0) trace_at(p.trace, 6000);
-  if (warp == kAllocWarp) tmem_alloc(tmem_slot, 512);
+  if (warp == kAllocWarp) {
+    if (PAIR)
+      tmem_alloc2(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();   // both CTAs' barriers initialised before any cross-CTA signal
   if (tracing && threadIdx.x == 0) trace_at(p.trace, 6001);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();                        // the next layer's kernel may launch and run its prologue
   if (warp != kProdWarp) pdl_wait();    // (the producer waits after issuing the resident weights)
 
-  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  // (PAIR: tiles, CTAs and grid counted in pairs; CTA rank r computes M tile 2 m + r)
+  const int num_tiles = (PAIR ? (p.num_m_tiles + 1) >> 1 : p.num_m_tiles) * p.num_n_tiles;
+  const int vbx = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, vgx = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const uint32_t full_l = PAIR ? cluster_addr(&full[0], 0) : 0u, bres_l = PAIR ? cluster_addr(bres_full, 0) : 0u,
+                 tempty_l = PAIR ? cluster_addr(&tempty[0], 0) : 0u;
   // tile t = m_blk * nn + n_blk, visited t = blockIdx.x, += gridDim.x: (m_blk, n_blk) advanced without division
   const int nn = p.num_n_tiles;
-  const int m_first = blockIdx.x / nn, n_first = blockIdx.x - m_first * nn;
-  const int m_step = gridDim.x / nn, n_step = gridDim.x - m_step * nn;
+  const int m_first = vbx / nn, n_first = vbx - m_first * nn;
+  const int m_step = vgx / nn, n_step = vgx - m_step * nn;
 #define QNN_NEXT_TILE()  \
   do {                   \
     n_blk += n_step;     \
@@ -218,14 +260,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // The whole warp runs the loop (warp-uniform control flow keeps coordinates and
     // descriptor addresses in uniform registers); one elected lane issues.
     const bool leader = elect_one();
-    if (b_res && blockIdx.x < num_tiles) {
+    if (b_res && vbx < num_tiles) {
       // weights are shared by every tile of this CTA: load them once
       if (leader) {
-        mbar_arrive_expect_tx(bres_full, (uint32_t)(p.num_kb * bparts) * b_bytes);
+        if (prank == 0) mbar_arrive_expect_tx(bres_full, (uint32_t)(p.num_kb * bparts) * b_bytes * (PAIR ? 2u : 1u));
         // (a CTA keeps one N tile for all its tiles: grid % num_n == 0, see the host plan;
         // split weights: part a's num_kb k-blocks, then part b's)
-        for (int kb = 0; kb < p.num_kb * bparts; ++kb)
-          tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, n_first * BN);
+        for (int kb = 0; kb < p.num_kb * bparts; ++kb) {
+          if (PAIR)
+            tma_load_2d_pair(sB + kb * b_bytes, &tmB, bres_l, kb * BK, n_first * BN + (int)prank * (BN / 2));
+          else
+            tma_load_2d(sB + kb * b_bytes, &tmB, bres_full, kb * BK, n_first * BN);
+        }
       }
       __syncwarp();
     }
@@ -237,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (p.a_rows) {
       // one box per (tile, channel chunk): input rows p_first - pt .. + a_nri, columns -pl .. + Wp
       const uint32_t bytes = (uint32_t)(p.a_nri * p.a_Wp * BK);
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = vbx; t < num_tiles; t += vgx) {
         const int n = (int)fdiv((uint32_t)m_blk, p.fdT), tt = m_blk - n * p.a_T;
         const int p_first = (int)fdiv((uint32_t)(tt * kGemmBM), p.fdWp);
         for (int kc = 0; kc < p.nchunks; ++kc) {
@@ -263,7 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // raw input rows for the builders: per output row the tile touches, its R filter rows
       // (zero outside the image: TMA OOB fill), one 4-D box each
       const uint32_t bytes = (uint32_t)p.a_nr * p.num_kb * p.a_rowlen;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = vbx; t < num_tiles; t += vgx) {
         const int r_first = (m_blk * kGemmBM) / p.Q;
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
@@ -282,8 +328,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         QNN_NEXT_TILE();
       }
     }
-    for (int t = (p.a_build || p.a_rows) ? num_tiles : blockIdx.x; t < num_tiles; t += gridDim.x) {   // done above
-      const int m0 = m_blk * kGemmBM;
+    for (int t = (p.a_build || p.a_rows) ? num_tiles : vbx; t < num_tiles; t += vgx) {   // done above
+      const int m0 = (PAIR ? 2 * m_blk + (int)prank : m_blk) * kGemmBM;   // (PAIR: this CTA's M tile)
       int an = 0, ah = 0, aw = 0;
       if (p.im2col) {
         const int pq = p.P * p.Q;
@@ -301,22 +347,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) {
           if (tracing && it_p < 2048) trace_at(p.trace, it_p);
-          mbar_arrive_expect_tx(&full[stage],
-                                (uint32_t)nk * ((b_res ? 0 : b_bytes * bparts) + (skip_a ? 0 : a_bytes)));
+          if (prank == 0)   // (PAIR: the leader's barrier counts both CTAs' bytes)
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * ((b_res ? 0 : b_bytes * bparts) + (skip_a ? 0 : a_bytes)) *
+                                                    (PAIR ? 2u : 1u));
+          const uint32_t fb = full_l + (uint32_t)stage * 8u;
           uint8_t* dA = sA + (size_t)stage * a_stage;
           uint8_t* dB = sB + (size_t)(stage * kps) * b_bytes * bparts;
           for (int t2 = 0; t2 < nk; ++t2, dA += a_bytes, dB += b_bytes * bparts) {
             const int kb = kb0 + t2;
             if (skip_a) {
             } else if (p.im2col) {
-              tma_load_im2col_4d(dA, &tmA, &full[stage], kc * BK, aw, ah, an, (uint16_t)(ks * p.dil_w),
-                                 (uint16_t)(kr * p.dil_h));
+              if (PAIR)
+                tma_load_im2col_4d_pair(dA, &tmA, fb, kc * BK, aw, ah, an, (uint16_t)(ks * p.dil_w),
+                                        (uint16_t)(kr * p.dil_h));
+              else
+                tma_load_im2col_4d(dA, &tmA, &full[stage], kc * BK, aw, ah, an, (uint16_t)(ks * p.dil_w),
+                                   (uint16_t)(kr * p.dil_h));
             } else {
-              tma_load_2d(dA, &tmA, &full[stage], kb * BK, m0);
+              if (PAIR)
+                tma_load_2d_pair(dA, &tmA, fb, kb * BK, m0);
+              else
+                tma_load_2d(dA, &tmA, &full[stage], kb * BK, m0);
             }
             if (!b_res) {
-              tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
-              if (SPLIT) tma_load_2d(dB + b_bytes, &tmB, &full[stage], (p.num_kb + kb) * BK, n_blk * BN);
+              if (PAIR) {
+                tma_load_2d_pair(dB, &tmB, fb, kb * BK, n_blk * BN + (int)prank * (BN / 2));
+              } else {
+                tma_load_2d(dB, &tmB, &full[stage], kb * BK, n_blk * BN);
+                if (SPLIT) tma_load_2d(dB + b_bytes, &tmB, &full[stage], (p.num_kb + kb) * BK, n_blk * BN);
+              }
             }
             if (++kc == p.nchunks) {
               kc = 0;
@@ -354,7 +413,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int m_blk = m_first, n_blk = n_first;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = vbx; t < num_tiles; t += vgx) {
       const int m0 = m_blk * kGemmBM;
       const int r_first = (int)fdiv((uint32_t)m0, p.fdQ);
       const int row = m0 + mi;
@@ -420,7 +479,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       QNN_NEXT_TILE();
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp && prank == 0) {   // (PAIR: the peer's MMA warp only allocates TMEM)
     // ------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; the elected lane issues every tcgen05.mma and its commits.
     const bool leader = elect_one();
@@ -441,7 +500,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // (interleaved per k-block) when streamed
     const uint32_t bsplit16 = SPLIT ? (b_res ? ((uint32_t)num_kb * b_bytes) >> 4 : b_bytes >> 4) : 0u;
     if (b_res) mbar_wait(bres_full, 0);
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = vbx; t < num_tiles; t += vgx, ++it) {
       const int acc = it & (nacc - 1);
       const uint32_t acc_phase = (it >> acc_log) & 1;
       if (tracing && leader && it < 100) trace_at(p.trace, 7200 + it);
@@ -462,9 +521,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (tracing && it_m < 2048) trace_at(p.trace, 2048 + it_m);
             const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage) + (uint32_t)(off0 * BK)) >> 4);
             const uint64_t bd = bdesc0 + (((uint32_t)kc * b_bytes) >> 4);
-            issue_mma<SPLIT>(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0, bsplit16);
+            issue_mma<SPLIT, PAIR>(ksteps, d_tmem, ad, bd, idesc, R_taps, S_taps, a_row16, a_col16, b_tap16, kc != 0,
+                                   bsplit16);
             if (tracing && it_m < 64) trace_at(p.trace, 6100 + it_m);   // all MMAs of the stage issued
-            umma_commit(&empty[stage]);
+            commit_x<PAIR>(&empty[stage]);
           }
           __syncwarp();
           ++it_m;
@@ -484,9 +544,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // descriptors advance by (byte offset >> 4) in the start-address field
           const uint64_t ad = adesc0 + (((uint32_t)(stage * a_stage)) >> 4);
           const uint64_t bd = bdesc0 + (((uint32_t)(b_res ? kb0 : stage * kps * bparts) * b_bytes) >> 4);
-          issue_mma<SPLIT>(ksteps, d_tmem, ad, bd, idesc, 1, nk, 0, a_bytes >> 4, (b_bytes * (b_res ? 1 : bparts)) >> 4,
+          issue_mma<SPLIT, PAIR>(ksteps, d_tmem, ad, bd, idesc, 1, nk, 0, a_bytes >> 4, (b_bytes * (b_res ? 1 : bparts)) >> 4,
                            kb0 != 0, bsplit16);
-          umma_commit(&empty[stage]);
+          commit_x<PAIR>(&empty[stage]);
         }
         __syncwarp();
         ++it_m;
@@ -495,7 +555,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           phase ^= 1;
         }
       }
-      if (leader) umma_commit(&tfull[acc]);
+      if (leader) commit_x<PAIR>(&tfull[acc]);   // (PAIR: both CTAs' epilogues)
       if (tracing && leader && it < 100) trace_at(p.trace, 7400 + it);
       __syncwarp();
     }
@@ -531,13 +591,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ResTerm rt_res{e.res_M, e.res_rsh, e.res_zp, MODE, e.res_s8};
     int m_blk = m_first, n_blk = n_first;
     if (nsets > 1) {   // single N tile: tile t is (t, 0)
-      m_blk = blockIdx.x + set * gridDim.x;
+      m_blk = vbx + set * vgx;
       n_blk = 0;
     }
     // the first N tile's parameters are staged before the loop by all 16 warps (a set may own
     // no tile at all); later N-tile changes only happen with one set, where all warps see them
-    for (int t = blockIdx.x + set * gridDim.x, it = set, first = 1; t < num_tiles || first;
-         t += nsets * gridDim.x, it += nsets, first = 0) {
+    for (int t = vbx + set * vgx, it = set, first = 1; t < num_tiles || first;
+         t += nsets * vgx, it += nsets, first = 0) {
       const int acc = it & (nacc - 1);
       const uint32_t acc_phase = (it >> acc_log) & 1;
       if (first || n_blk != cur_n) {
@@ -589,7 +649,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cur_n = nb;
         if (t >= num_tiles) break;   // staged for the other sets only
       }
-      const int row0 = m_blk * kGemmBM + quad * 32;
+      const int row0 = (PAIR ? 2 * m_blk + (int)prank : m_blk) * kGemmBM + quad * 32;
       int row = row0 + lane;
       bool row_ok = row < p.M;
       int cls = 0;
@@ -637,7 +697,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (tracing && warp == 0 && lane == 0 && it < 500) trace_at(p.trace, 12000 + it * 8 + 0);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) release_acc<PAIR>(tempty, acc, tempty_l);
         if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
         if (lane == 0) bulk_wait_read<kEpiStageBufs - 1>();
         __syncwarp();
@@ -667,7 +727,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (dbg & 32) {   // (instrumented builds) no epilogue work: release the accumulator at once
         tc_fence_before();
         __syncwarp();
-        if (lane == 0 && c_begin < c_end) mbar_arrive(&tempty[acc]);
+        if (lane == 0 && c_begin < c_end) release_acc<PAIR>(tempty, acc, tempty_l);
       }
 #pragma unroll 1
       for (int j = (two || (dbg & 32)) ? c_end : c_begin; j < c_end; ++j) {
@@ -677,7 +737,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // accumulator fully read by this warp: hand the TMEM buffer back to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) release_acc<PAIR>(tempty, acc, tempty_l);
           if (tracing && lane == 0 && it < 100) trace_at(p.trace, 7500 + it * 16 + warp);
         }
         const int k0 = n_blk * BN + j * 32;
@@ -781,10 +841,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (c_begin == c_end) {  // no columns for this warp: still release the accumulator
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) release_acc<PAIR>(tempty, acc, tempty_l);
       }
       if (nsets > 1)
-        m_blk += nsets * gridDim.x;
+        m_blk += nsets * vgx;
       else
         QNN_NEXT_TILE();
     }
@@ -796,19 +856,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (tracing && threadIdx.x == 0) trace_at(p.trace, 6002);
+  if (PAIR) cluster_sync_all();   // the peer's last signals target this CTA; TMEM is the pair's
   if (warp == kAllocWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (PAIR)
+      tmem_dealloc2(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR>
 static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                   const GemmParams& p, int grid, cudaStream_t stream) {
   static int attr_done[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT, RES, SPLIT>;
+  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT, RES, SPLIT, PAIR>;
   if (dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
@@ -816,10 +880,28 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   }
   constexpr int bparts = SPLIT ? 2 : 1;
   const size_t smem = gemm_smem_bytes(p.BK, p.BN, p.stages, HAS_CLS ? p.e.ncls : 1, p.b_res ? p.num_kb * bparts : 0,
-                                      p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts, p.out_staging != 0);
+                                      p.kps, p.a_raw_bytes, p.a_stage_bytes, bparts, p.out_staging != 0, PAIR);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, stream, tmA, tmB, tmC[0], tmC[1], tmC[2],
-                             tmC[3], p);
+  if (PAIR) {   // as many CTA pairs as can be co-resident (GPCs with odd SM counts), grid / 2 a multiple of num_n
+    static int maxc[64] = {0};
+    static size_t maxc_smem[64] = {0};
+    int m = 0;
+    if (dev < 64 && maxc_smem[dev] == smem) {
+      m = maxc[dev];
+    } else {
+      m = max_active_clusters(kern, dim3(kGemmThreads), smem, 2);
+      if (dev < 64) {
+        maxc[dev] = m;
+        maxc_smem[dev] = smem;
+      }
+    }
+    int pairs = std::min(grid / 2, m);
+    pairs -= pairs % p.num_n_tiles;
+    if (pairs <= 0) return cudaErrorInvalidValue;
+    grid = 2 * pairs;
+  }
+  cudaError_t e = launch_ex(kern, dim3(grid), dim3(kGemmThreads), smem, stream, PAIR ? 2 : 1, tmA, tmB, tmC[0],
+                            tmC[1], tmC[2], tmC[3], p);
   count_launch();
   if (e == cudaSuccess) e = cudaGetLastError();
   static const bool trace_err = std::getenv("QNN_PLAN_TRACE") != nullptr;
@@ -829,8 +911,9 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   return e;
 }
 
-// one translation unit per SPLIT value (gemm_sm100.cu, gemm_sm100_split.cu): compiled in parallel
-template <bool SPLIT>
+// one translation unit per (SPLIT, PAIR) variant (gemm_sm100.cu, gemm_sm100_split.cu,
+// gemm_sm100_pair.cu): compiled in parallel
+template <bool SPLIT, bool PAIR>
 static cudaError_t launch_gemm_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                     const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream) {
   const bool cls = p.e.ncls > 1;
@@ -838,7 +921,7 @@ static cudaError_t launch_gemm_impl(const CUtensorMap& tmA, const CUtensorMap& t
   const bool res = p.e.res != nullptr && mode != 2;
 #define QNN_GEMM_CASE(M_, C_, K_, S_, R_)                            \
   if (mode == M_ && cls == C_ && clamp == K_ && s8 == S_ && res == R_) \
-    return launch_variant<M_, C_, K_, S_, R_, SPLIT>(tmA, tmB, tmC, p, grid, stream);
+    return launch_variant<M_, C_, K_, S_, R_, SPLIT, PAIR>(tmA, tmB, tmC, p, grid, stream);
 #define QNN_GEMM_CASES(M_, C_, K_)                                                            \
   QNN_GEMM_CASE(M_, C_, K_, false, false) QNN_GEMM_CASE(M_, C_, K_, true, false)              \
   QNN_GEMM_CASE(M_, C_, K_, false, true) QNN_GEMM_CASE(M_, C_, K_, true, true)

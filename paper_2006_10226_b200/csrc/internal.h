@@ -146,6 +146,7 @@ struct GemmParams {
   GemmEpilogue e;
   int wsplit; // weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction)
   int out_staging;  // the epilogue's TMA-store staging region is allocated (0: direct stores only)
+  int pair;         // CTA pairs (cta_group::2): consecutive M tiles of a cluster of 2 form one M = 256 MMA
 };
 
 // Launch with programmatic stream serialization (PDL) so the kernel's prologue (barrier init,
@@ -230,15 +231,18 @@ __host__ __device__ inline int gemm_epi_sets(int BN, int num_n_tiles, int nepi =
 }
 
 // epilogue variants: MODE 0 = requantize UPWARD, 1 = requantize TONEAREST, 2 = raw int32
-// out_staging = false: no TMA-store staging region (plans whose epilogue stores directly)
+// out_staging = false: no TMA-store staging region (plans whose epilogue stores directly);
+// pair: CTA-pair plans (each CTA stages half of each B k-block)
 size_t gemm_smem_bytes(int BK, int BN, int stages, int ncls, int b_res_kb, int kps, int raw_bytes = 0,
-                       int a_stage_bytes = 0, int bparts = 1, bool out_staging = true);
+                       int a_stage_bytes = 0, int bparts = 1, bool out_staging = true, bool pair = false);
 int gemm_max_stages(int BK, int BN, int ncls, int b_res_kb, int kps, int raw_bytes = 0, int a_stage_bytes = 0,
-                    int bparts = 1, bool out_staging = true);
+                    int bparts = 1, bool out_staging = true, bool pair = false);
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                         const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 cudaError_t launch_gemm_split(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                               const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
+cudaError_t launch_gemm_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
+                             const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // Prepack / auxiliary kernels (prep.cu)

@@ -607,3 +607,17 @@ print("OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_PAIR="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+def test_pixel_major_cta_pair_subprocess():
+    """QNN_PAIR=1 also turns on the pixel-major kernel's CTA-pair variants (cta_group::2: the two
+    M tiles of a cluster form one M = 256 MMA, each CTA staging half of the weight tile): strided
+    3x3 (im2col), stride-1 3x3, strided 1x1, BN = 192 / 256, a dense with int32 output, both
+    rounding modes, ragged M tails -- bit-exact against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "tools/pair_quick_pm.py"], cwd=root, env=dict(os.environ, QNN_PAIR="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), (r.stdout[-2000:], r.stderr[-2000:])
