@@ -18,7 +18,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-RUN = os.path.join(ROOT, "gpurun_out", "r02prof")
+RUN = os.environ.get("R02_RUN") or os.path.join(ROOT, "gpurun_out", "r02prof")
 OUT = os.path.join(ROOT, "profiles")
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 from summarize_profiles import load_launches, short  # noqa: E402
