@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.environ.get("QNN_LIB_OUT") or os.path.join(PKG, "libqnn.so")
-SOURCES = ["abi.cu", "gemm_sm100.cu", "gemm_sm100_split.cu", "gemm_sm100_pair.cu", "gemm_t.cu", "prep.cu", "depthwise.cu", "depthwise_tc.cu", "depthwise_tma.cu", "elementwise.cu", "glue.cu"]
+SOURCES = ["abi.cu", "gemm_sm100.cu", "gemm_sm100_split.cu", "gemm_sm100_pair.cu", "gemm_sm100_arows.cu", "gemm_t.cu", "prep.cu", "depthwise.cu", "depthwise_tc.cu", "depthwise_tma.cu", "elementwise.cu", "glue.cu"]
 HEADERS = ["common.cuh", "epilogue.cuh", "internal.h", "gemm_sm100.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

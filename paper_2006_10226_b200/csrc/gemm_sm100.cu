@@ -35,7 +35,8 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
                         int mode, bool clamp, int grid, cudaStream_t stream) {
   if (p.wsplit) return launch_gemm_split(tmA, tmB, tmC, p, mode, clamp, grid, stream);
   if (p.pair) return launch_gemm_pair(tmA, tmB, tmC, p, mode, clamp, grid, stream);
-  return launch_gemm_impl<false, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  if (p.a_rows) return launch_gemm_arows(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  return launch_gemm_impl<false, false, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
 }
 
 }  // namespace qnn

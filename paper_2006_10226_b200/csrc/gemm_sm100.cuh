@@ -146,7 +146,7 @@ __device__ __forceinline__ void issue_mma(int ksteps, uint32_t d, uint64_t ad, u
     issue_mma_ks<1, SPLIT, PAIR>(d, ad, bd, idesc, R, S, a_row16, a_col16, b_tap16, acc, bsplit16);
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR, bool AROWS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     qnn_gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     const bool skip_a = dbg & 4;
     int m_blk = m_first, n_blk = n_first;
-    if (p.a_rows) {
+    if (AROWS) {
       // one box per (tile, channel chunk): input rows p_first - pt .. + a_nri, columns -pl .. + Wp
       const uint32_t bytes = (uint32_t)(p.a_nri * p.a_Wp * BK);
       for (int t = vbx; t < num_tiles; t += vgx) {
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         QNN_NEXT_TILE();
       }
     }
-    for (int t = (p.a_build || p.a_rows) ? num_tiles : vbx; t < num_tiles; t += vgx) {   // done above
+    for (int t = (p.a_build || AROWS) ? num_tiles : vbx; t < num_tiles; t += vgx) {   // done above
       const int m0 = (PAIR ? 2 * m_blk + (int)prank : m_blk) * kGemmBM;   // (PAIR: this CTA's M tile)
       int an = 0, ah = 0, aw = 0;
       if (p.im2col) {
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ksteps = (dbg & 8) ? 0 : BK / 32;
     // loop-invariant issue parameters in registers (tight issue loops: see issue_mma)
     const uint32_t idesc = p.idesc;
-    const bool a_rows = p.a_rows;
+    constexpr bool a_rows = AROWS;
     const int nchunks = p.nchunks, num_kb = p.num_kb;
     const int S_taps = a_rows ? p.S : 1, R_taps = a_rows ? num_kb / (p.S * nchunks) : 1;
     const uint32_t a_col16 = (uint32_t)BK >> 4, a_row16 = (uint32_t)(p.a_Wp * BK) >> 4;
@@ -598,6 +598,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // no tile at all); later N-tile changes only happen with one set, where all warps see them
     for (int t = vbx + set * vgx, it = set, first = 1; t < num_tiles || first;
          t += nsets * vgx, it += nsets, first = 0) {
+      if (nsets > 1) m_blk = t;   // (several sets: single N tile, tile t is (t, 0); not carried)
       const int acc = it & (nacc - 1);
       const uint32_t acc_phase = (it >> acc_log) & 1;
       if (first || n_blk != cur_n) {
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       bool row_ok = row < p.M;
       int cls = 0;
       int32_t rterm = 0;
-      if (p.a_rows) {
+      if (AROWS) {
         // flattened (p, q) with pitch Wp per image: q >= Q (and rows past P) are discarded
         const int n = (int)fdiv((uint32_t)m_blk, p.fdT), tt = m_blk - n * p.a_T;
         const int f = tt * kGemmBM + quad * 32 + lane;
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         row = (n * p.P + pp) * p.Q + qq;
         if (row_ok) {
           if (HAS_CLS) cls = (int)e.rowcls[pp] * e.ncc + (int)e.colcls[qq];
-          if (e.rowsum) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
+          if (has_rt) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
         }
       } else if (row_ok) {
         if (HAS_CLS) {
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int pp = (int)fdiv((uint32_t)rem, p.fdQ), qq = rem - pp * p.Q;
           cls = (int)e.rowcls[pp] * e.ncc + (int)e.colcls[qq];
         }
-        if (e.rowsum) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
+        if (has_rt) rterm = (int32_t)((uint32_t)e.zpW * (uint32_t)e.rowsum[row]);
       }
       uint8_t* stage_out = stage_base + sbuf * 2048;
       if (tracing && warp == 0 && lane == 0 && it < 512) trace_at(p.trace, 4096 + it);
@@ -843,10 +844,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) release_acc<PAIR>(tempty, acc, tempty_l);
       }
-      if (nsets > 1)
-        m_blk += nsets * vgx;
-      else
-        QNN_NEXT_TILE();
+      if (nsets == 1) QNN_NEXT_TILE();
     }
     if (tma_st && lane == 0) bulk_wait_all();
     __syncwarp();
@@ -866,13 +864,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR>
+template <int MODE, bool HAS_CLS, bool CLAMP, bool S8OUT, bool RES, bool SPLIT, bool PAIR, bool AROWS>
 static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                   const GemmParams& p, int grid, cudaStream_t stream) {
   static int attr_done[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT, RES, SPLIT, PAIR>;
+  auto kern = qnn_gemm_i8_kernel<MODE, HAS_CLS, CLAMP, S8OUT, RES, SPLIT, PAIR, AROWS>;
   if (dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
@@ -911,9 +909,10 @@ static cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB
   return e;
 }
 
-// one translation unit per (SPLIT, PAIR) variant (gemm_sm100.cu, gemm_sm100_split.cu,
-// gemm_sm100_pair.cu): compiled in parallel
-template <bool SPLIT, bool PAIR>
+// one translation unit per (SPLIT, PAIR, AROWS) variant (gemm_sm100.cu, gemm_sm100_split.cu,
+// gemm_sm100_pair.cu, gemm_sm100_arows.cu): compiled in parallel; each kernel carries only its
+// own operand-staging path (the 96-register budget: code of another path costs spills)
+template <bool SPLIT, bool PAIR, bool AROWS>
 static cudaError_t launch_gemm_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                                     const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream) {
   const bool cls = p.e.ncls > 1;
@@ -921,7 +920,7 @@ static cudaError_t launch_gemm_impl(const CUtensorMap& tmA, const CUtensorMap& t
   const bool res = p.e.res != nullptr && mode != 2;
 #define QNN_GEMM_CASE(M_, C_, K_, S_, R_)                            \
   if (mode == M_ && cls == C_ && clamp == K_ && s8 == S_ && res == R_) \
-    return launch_variant<M_, C_, K_, S_, R_, SPLIT, PAIR>(tmA, tmB, tmC, p, grid, stream);
+    return launch_variant<M_, C_, K_, S_, R_, SPLIT, PAIR, AROWS>(tmA, tmB, tmC, p, grid, stream);
 #define QNN_GEMM_CASES(M_, C_, K_)                                                            \
   QNN_GEMM_CASE(M_, C_, K_, false, false) QNN_GEMM_CASE(M_, C_, K_, true, false)              \
   QNN_GEMM_CASE(M_, C_, K_, false, true) QNN_GEMM_CASE(M_, C_, K_, true, true)

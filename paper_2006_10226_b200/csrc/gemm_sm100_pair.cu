@@ -8,7 +8,7 @@ namespace qnn {
 
 cudaError_t launch_gemm_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                              const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream) {
-  return launch_gemm_impl<false, true>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  return launch_gemm_impl<false, true, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
 }
 
 }  // namespace qnn

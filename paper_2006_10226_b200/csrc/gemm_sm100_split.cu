@@ -8,7 +8,9 @@ namespace qnn {
 
 cudaError_t launch_gemm_split(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                               const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream) {
-  return launch_gemm_impl<true, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
+  // (split weights on staged-row plans included: the AROWS path is a runtime choice there)
+  return p.a_rows ? launch_gemm_impl<true, false, true>(tmA, tmB, tmC, p, mode, clamp, grid, stream)
+                  : launch_gemm_impl<true, false, false>(tmA, tmB, tmC, p, mode, clamp, grid, stream);
 }
 
 }  // namespace qnn

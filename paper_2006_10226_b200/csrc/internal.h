@@ -243,6 +243,8 @@ cudaError_t launch_gemm_split(const CUtensorMap& tmA, const CUtensorMap& tmB, co
                               const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 cudaError_t launch_gemm_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
                              const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
+cudaError_t launch_gemm_arows(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap* tmC,
+                              const GemmParams& p, int mode, bool clamp, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // Prepack / auxiliary kernels (prep.cu)
