@@ -1208,6 +1208,17 @@ static qnn_status_t conv_packed(const qnn_conv2d_desc_t* d, const qnn_output_par
                           pl.pair ? 2 * kGemmBM : kGemmBM, pl.BN);   // (a pair's MMA has M = 256)
   p.wsplit = pl.wsplit;
   p.pair = pl.pair ? 1 : 0;
+  {
+    // staged-row plans store directly (no TMA store) and their epilogue is the bound: four warp
+    // sets on alternate tiles (one quad each, every column chunk) keep four tiles' epilogues in
+    // flight (ResNet-50 b256 layer2 3x3 s1 47 -> 39 us, layer1 3x3 58 -> 55 us; needs 4
+    // accumulators: BN <= 128).  QNN_EPI_SETS=1/2/4 overrides (A/B measurements).
+    static const int es_env = std::getenv("QNN_EPI_SETS") ? std::atoi(std::getenv("QNN_EPI_SETS")) : 0;
+    const int es = es_env ? es_env : 4;
+    if (pl.a_rows && pl.num_n == 1 && (es == 1 || es == 2 || es == 4) && pl.BN / 32 >= 4 / es &&
+        gemm_acc_bufs(pl.BN) >= es)
+      p.epi_sets = es;
+  }
   GemmEpilogue& ep = p.e;
   ep.off = reinterpret_cast<const int32_t*>(pk + pl.pk_off);
   ep.off64 = reinterpret_cast<const int64_t*>(pk + pl.pk_off64);

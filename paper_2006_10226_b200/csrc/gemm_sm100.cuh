@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t acc_cols = 512u / nacc;
   // a_build: warps 8..15 build A tiles, warps 0..7 run the epilogue
   const int nepi = p.a_build ? 8 : kGemmEpiWarps;
-  const int nsets = gemm_epi_sets(BN, p.num_n_tiles, nepi);
+  const int nsets = p.epi_sets ? p.epi_sets : gemm_epi_sets(BN, p.num_n_tiles, nepi);
   // PAIR (cta_group::2, clusters of 2): the pair's two M tiles form one M = 256 MMA issued by the
   // leader (rank 0); each CTA stages its own A tile and half of the B tile (BN / 2 rows); TMA
   // loads of both CTAs complete on the leader's barriers, commits reach both CTAs, every

@@ -146,6 +146,7 @@ struct GemmParams {
   GemmEpilogue e;
   int wsplit; // weights packed as W - zp_W[k] in two s8 parts (Term 3 in the contraction)
   int out_staging;  // the epilogue's TMA-store staging region is allocated (0: direct stores only)
+  int epi_sets;     // epilogue warp sets taking alternate tiles (0: gemm_epi_sets; single N tile only)
   int pair;         // CTA pairs (cta_group::2): consecutive M tiles of a cluster of 2 form one M = 256 MMA
 };
 
