@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         const int acc = set;
         QNN_TEPI_WAIT(&tfull[acc], (it >> 1) & 1);
         tc_fence_after();
+        if ((warp & 7) == 0 && lane == 0) t_trace(p.trace, 320, it);   // (warps 0 / 8: one per set)
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           const int colrel = sg * (2 * kTCols) + c * kTCols;
@@ -590,12 +591,14 @@ __global__ void __launch_bounds__(kTThreads, 1)
           named_bar_sync(1 + grp, 32 * ep_quads);
           const uint32_t tb = tmem_base + (uint32_t)acc * kTBN + ((uint32_t)(quad * 32) << 16) + (uint32_t)colrel;
           uint32_t va0[16], vb0[16], va1[16], vb1[16];
-          tmem_ld_16x256b_x4(tb, va0);
-          tmem_ld_16x256b_x4(tb + (16u << 16), vb0);
-          tmem_ld_16x256b_x4(tb + 32, va1);
-          tmem_ld_16x256b_x4(tb + 32 + (16u << 16), vb1);
-          tmem_wait16x2(va0, vb0);
-          tmem_wait16x2(va1, vb1);
+          if (!(dbg & 16)) {   // (instrumented builds: 16 skips the TMEM loads)
+            tmem_ld_16x256b_x4(tb, va0);
+            tmem_ld_16x256b_x4(tb + (16u << 16), vb0);
+            tmem_ld_16x256b_x4(tb + 32, va1);
+            tmem_ld_16x256b_x4(tb + 32 + (16u << 16), vb1);
+            tmem_wait16x2(va0, vb0);
+            tmem_wait16x2(va1, vb1);
+          }
           tc_fence_before();
           __syncwarp();
           if (c == 1 && lane == 0) {   // this warp is done with the accumulator
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
             else
               mbar_arrive(&tempty[acc]);
           }
-          if (!quad_live) {
+          if (!quad_live || (dbg & 1)) {   // (instrumented builds: 1 skips the math)
           } else if (all_fast) {
             t_epilogue<MODE, true, CLAMP, S8OUT, false>(p, q, va0, vb0, sbase + st_off0, sbase + st_off1, out_rb);
             t_epilogue<MODE, true, CLAMP, S8OUT, false>(p, q, va1, vb1, sbase + 32 * out_rb + st_off0,
@@ -616,11 +619,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
           }
           fence_proxy_async_smem();
           named_bar_sync(1 + grp, 32 * ep_quads);
-          if (gleader) {
+          if (gleader && !(dbg & 2)) {   // (instrumented builds: 2 skips the stores)
             tma_store_2d(&tmC, stage_out, ch * kTBM, pt * kTBN + colrel);
             bulk_commit();
           }
         }
+        if ((warp & 7) == 0 && lane == 0) t_trace(p.trace, 384, it);
       }
     }
     int it = 0;
