@@ -269,6 +269,132 @@ __global__ void __launch_bounds__(256) pool16_kernel(const __grid_constant__ Poo
   }
 }
 
+
+// 3x3 pooling with stride SH (1 or 2), separable: a thread owns 16 channels of one output
+// column and sweeps a band of BP output rows; each input row is loaded once (3 x 16 B) and
+// reduced across its 3 columns into 16-bit lanes (even / odd bytes: VIMNMX.U16x2 for max,
+// VIADD.16x2 for sums, one instruction per 2 lanes), and an output row combines the row
+// reductions of its 3 input rows -- kept in registers across output rows (stride 1 reuses 2
+// of them, stride 2 one).  Same results as pool16_kernel (max of the valid taps; average =
+// valid-tap sum / count rounded half away from zero, reading R20).
+constexpr int kP3Band = 8;
+__device__ __forceinline__ void p3_split(const uint4 v4, uint32_t bias, uint32_t (&lo)[4], uint32_t (&hi)[4]) {
+  const uint32_t v[4] = {v4.x ^ bias, v4.y ^ bias, v4.z ^ bias, v4.w ^ bias};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    lo[k] = v[k] & 0x00FF00FFu;
+    hi[k] = (v[k] >> 8) & 0x00FF00FFu;
+  }
+}
+template <bool AVG>
+__device__ __forceinline__ void p3_row(const uint8_t* rowp, long long cs, int w0, int W, bool rok, uint32_t bias,
+                                       uint32_t (&red)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[k] = 0u;   // (max identity: 0 in the biased unsigned domain)
+  if (!rok) return;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int w = w0 + s;
+    if (w < 0 || w >= W) continue;
+    uint32_t lo[4], hi[4];
+    p3_split(__ldg(reinterpret_cast<const uint4*>(rowp + (long long)w * cs)), bias, lo, hi);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      red[k] = AVG ? __vadd2(red[k], lo[k]) : __vmaxu2(red[k], lo[k]);
+      red[k + 4] = AVG ? __vadd2(red[k + 4], hi[k]) : __vmaxu2(red[k + 4], hi[k]);
+    }
+  }
+}
+
+template <bool S8, bool AVG, int SH>
+__global__ void __launch_bounds__(256) pool3_kernel(const __grid_constant__ PoolParams p, FastDiv fdG, FastDiv fdQ,
+                                                    FastDiv fdB) {
+  pdl_wait();      // inputs are the previous kernel's output (PDL launch; no early trigger)
+  const int G = p.C >> 4;
+  const int NB = (p.P + kP3Band - 1) / kP3Band;
+  const uint32_t total = (uint32_t)p.N * NB * p.Q * G;
+  const uint8_t* in = reinterpret_cast<const uint8_t*>(p.in);
+  uint8_t* out = reinterpret_cast<uint8_t*>(p.out);
+  const uint32_t bias = S8 ? 0x80808080u : 0u;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t r0 = fdiv(idx, fdG);
+    const int g = (int)(idx - r0 * G);
+    const uint32_t r1 = fdiv(r0, fdQ);
+    const int q = (int)(r0 - r1 * p.Q);
+    const uint32_t n = fdiv(r1, fdB);
+    const int b = (int)(r1 - n * NB);
+    const int p0 = b * kP3Band, p1 = min(p.P, p0 + kP3Band);
+    const int w0 = q * SH - p.pl;
+    int cols = 0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) cols += (w0 + s >= 0 && w0 + s < p.W) ? 1 : 0;
+    const uint8_t* base = in + (long long)n * p.H * p.W * p.in_cs + g * 16;
+    uint8_t* obase = out + ((long long)n * p.P * p.Q + q) * p.out_cs + g * 16;
+    uint32_t R0[8], R1[8], R2[8];
+    int h = p0 * SH - p.pt;   // first input row of output row p0
+    bool v0 = (unsigned)h < (unsigned)p.H, v1 = (unsigned)(h + 1) < (unsigned)p.H,
+         v2 = (unsigned)(h + 2) < (unsigned)p.H;
+    p3_row<AVG>(base + (long long)h * p.W * p.in_cs, p.in_cs, w0, p.W, v0, bias, R0);
+    p3_row<AVG>(base + (long long)(h + 1) * p.W * p.in_cs, p.in_cs, w0, p.W, v1, bias, R1);
+    p3_row<AVG>(base + (long long)(h + 2) * p.W * p.in_cs, p.in_cs, w0, p.W, v2, bias, R2);
+    for (int pp = p0; pp < p1; ++pp) {
+      if (pp > p0) {   // slide the window SH input rows down
+        h += SH;
+        if (SH == 1) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            R0[k] = R1[k];
+            R1[k] = R2[k];
+          }
+          v0 = v1;
+          v1 = v2;
+          v2 = (unsigned)(h + 2) < (unsigned)p.H;
+          p3_row<AVG>(base + (long long)(h + 2) * p.W * p.in_cs, p.in_cs, w0, p.W, v2, bias, R2);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) R0[k] = R2[k];
+          v0 = v2;
+          v1 = (unsigned)(h + 1) < (unsigned)p.H;
+          v2 = (unsigned)(h + 2) < (unsigned)p.H;
+          p3_row<AVG>(base + (long long)(h + 1) * p.W * p.in_cs, p.in_cs, w0, p.W, v1, bias, R1);
+          p3_row<AVG>(base + (long long)(h + 2) * p.W * p.in_cs, p.in_cs, w0, p.W, v2, bias, R2);
+        }
+      }
+      uint32_t ow[4];
+      if (AVG) {
+        const int cnt = ((int)v0 + (int)v1 + (int)v2) * cols;
+        const uint32_t mag = div_magic(2u * (uint32_t)(cnt > 0 ? cnt : 1));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t slo = __vadd2(__vadd2(R0[k], R1[k]), R2[k]), shi = __vadd2(__vadd2(R0[k + 4], R1[k + 4]), R2[k + 4]);
+          uint32_t bytes = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {   // byte j of the word: lane j >> 1 of lo (even j) / hi (odd j)
+            const uint32_t word = (j & 1) ? shi : slo;
+            int32_t sum = (int32_t)((word >> (16 * (j >> 1))) & 0xFFFFu);
+            if (S8) sum -= 128 * cnt;
+            int32_t y = 0;
+            if (cnt > 0) {
+              const uint32_t a = (uint32_t)(sum < 0 ? -sum : sum);
+              const int32_t m = (int32_t)div_small(2u * a + (uint32_t)cnt, mag);
+              y = sum < 0 ? -m : m;
+            }
+            bytes |= ((uint32_t)y & 0xFFu) << (8 * j);
+          }
+          ow[k] = bytes;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t mlo = __vmaxu2(__vmaxu2(R0[k], R1[k]), R2[k]), mhi = __vmaxu2(__vmaxu2(R0[k + 4], R1[k + 4]), R2[k + 4]);
+          ow[k] = (mlo | (mhi << 8)) ^ bias;
+        }
+      }
+      *reinterpret_cast<uint4*>(obase + (long long)pp * p.Q * p.out_cs) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+  }
+}
+
 cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -279,6 +405,22 @@ cudaError_t launch_pool(const PoolParams& p, cudaStream_t s) {
   // most 128 taps fit the 16-bit lanes, and the work-item count fits 32 bits
   constexpr int kTQ = 4;
   const long long items = (long long)p.N * p.P * ((p.Q + kTQ - 1) / kTQ) * (p.C / 16);
+  // 3x3, stride 1 / 2 (ResNet-50 stem max pool, Inception-v3 max / branch average pools): the
+  // separable row-reduction kernel (QNN_POOL_NO3=1 keeps pool16, A/B measurements)
+  static const bool no3 = std::getenv("QNN_POOL_NO3") != nullptr;
+  const long long items3 = (long long)p.N * ((p.P + kP3Band - 1) / kP3Band) * p.Q * (p.C / 16);
+  if (!no3 && v16 && p.R == 3 && p.S == 3 && p.sh == p.sw && (p.sh == 1 || p.sh == 2) && items3 < (1ll << 31)) {
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((items3 + 255) / 256, (long long)sms * 16));
+    const FastDiv fdG = make_fastdiv((uint32_t)(p.C / 16)), fdQ = make_fastdiv((uint32_t)p.Q),
+                  fdB = make_fastdiv((uint32_t)((p.P + kP3Band - 1) / kP3Band));
+#define QNN_POOL3(S_, A_, H_) \
+  if (p.s8 == S_ && p.avg == A_ && p.sh == H_) launch_pdl(pool3_kernel<S_, A_, H_>, dim3(blocks), dim3(256), 0, s, p, fdG, fdQ, fdB);
+    QNN_POOL3(false, false, 1) QNN_POOL3(false, true, 1) QNN_POOL3(true, false, 1) QNN_POOL3(true, true, 1)
+    QNN_POOL3(false, false, 2) QNN_POOL3(false, true, 2) QNN_POOL3(true, false, 2) QNN_POOL3(true, true, 2)
+#undef QNN_POOL3
+    count_launch();
+    return cudaGetLastError();
+  }
   if (v16 && p.R * p.S <= 128 && items < (1ll << 31)) {
     const int blocks = (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, (long long)sms * 16));
     const FastDiv fdG = make_fastdiv((uint32_t)(p.C / 16)), fdQB = make_fastdiv((uint32_t)((p.Q + kTQ - 1) / kTQ)),
