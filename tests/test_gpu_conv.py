@@ -521,9 +521,11 @@ print("OK")
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
 
 
-def test_two_mma_issuers_subprocess():
-    """QNN_MMA2=1: two MMA-issuing warps on alternate tiles, each with half of the stage ring
-    (stride-1 staged rows, im2col with streamed weights, 1x1 with resident weights)."""
+@pytest.mark.parametrize("sets", ["1", "2", "4"])
+def test_staged_row_epilogue_sets_subprocess(sets):
+    """QNN_EPI_SETS=1/2/4: the staged-row plans' epilogue warp sets on alternate tiles (4 is the
+    default) -- stride-1 staged rows at BN 64 / 128 with ragged tails, plus an im2col and a
+    1x1 shape that keep their own plans."""
     import os
     import subprocess
     import sys
@@ -532,8 +534,8 @@ import sys, numpy as np
 sys.path.insert(0, "tests")
 from gpu_helpers import gpu_conv, oracle_conv
 from workloads import gen
-cfgs = [(4, 64, 20, 19, 64, 3, 3, (1, 1), (1, 1, 1, 1)), (3, 128, 17, 15, 128, 3, 3, (2, 2), (1, 1, 1, 1)),
-        (4, 256, 14, 13, 64, 1, 1, (1, 1), (0, 0, 0, 0))]
+cfgs = [(4, 64, 20, 19, 64, 3, 3, (1, 1), (1, 1, 1, 1)), (3, 128, 17, 15, 128, 3, 3, (1, 1), (1, 1, 1, 1)),
+        (3, 128, 17, 15, 128, 3, 3, (2, 2), (1, 1, 1, 1)), (4, 256, 14, 13, 64, 1, 1, (1, 1), (0, 0, 0, 0))]
 for i, (N, C, H, W, K, R, S, st, pad) in enumerate(cfgs):
     case = gen.conv_case(1800 + i, N, C, H, W, K, R, S, st, pad, (1, 1), 1, "u8", "s8")
     _, _, y = gpu_conv(case)
@@ -541,7 +543,7 @@ for i, (N, C, H, W, K, R, S, st, pad) in enumerate(cfgs):
 print("OK")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_MMA2="1"),
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QNN_EPI_SETS=sets),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
 
