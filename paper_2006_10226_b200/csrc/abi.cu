@@ -589,7 +589,13 @@ static qnn_status_t make_plan(const qnn_conv2d_desc_t* d, const qnn_output_param
     // those layers pixel-major
     static const bool no_trans = std::getenv("QNN_NO_TRANS") != nullptr;
     static const int kTransMinK = std::getenv("QNN_TRANS_MINK") ? std::atoi(std::getenv("QNN_TRANS_MINK")) : 64;
-    if (!no_trans && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows && d->groups == 1 &&
+    // (small M: when the channel-major grid of 256-pixel x 128-channel tiles would leave most
+    // SMs idle and the pixel-major plan has more tiles, keep the pixel-major plan -- the
+    // per-GPU batch 32 of 8-GPU strong scaling; QNN_TRANS_SMALLM=1 disables the check)
+    static const bool small_ok = std::getenv("QNN_TRANS_SMALLM") != nullptr;
+    const long long t_tiles = ((pl.M + kGemmTBN - 1) / kGemmTBN) * ((d->K + 127) / 128);
+    const bool few = !small_ok && t_tiles < sm_count() / 2 && (long long)pl.num_m * pl.num_n > t_tiles;
+    if (!no_trans && !few && !pl.im2col && !pl.fold && !pl.pad_copy && !pl.a_build && !pl.a_rows && d->groups == 1 &&
         (!pl.any_zpw || pl.wsplit) && (d->kernel_dtype == QNN_S8 || pl.wsplit) && pl.requant &&
         (pl.out_dt == QNN_U8 || pl.out_dt == QNN_S8) && (d->K % 128 == 0 || d->K == 64) && d->K >= kTransMinK &&
         pl.out_cs % 16 == 0 && pl.ct.ncr * pl.ct.ncc == 1) {
